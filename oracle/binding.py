@@ -87,13 +87,14 @@ class CpuKpme:
             raise FileNotFoundError(f"{path} not built (run __graft_entry__.build())")
         self.which = which
         self.lib = C.CDLL(path)
-        self.lib[self.pfx + "last_error"].restype = C.c_char_p
-        self.lib[self.pfx + "alpha_weight"].restype = C.c_double
-        self.lib[self.pfx + "optimal_term_lower_bound"].restype = C.c_longlong
-        self.lib[self.pfx + "op_count_estimate"].restype = C.c_longlong
+        # attribute access caches the function object, so restype sticks
+        self._f("last_error").restype = C.c_char_p
+        self._f("alpha_weight").restype = C.c_double
+        self._f("optimal_term_lower_bound").restype = C.c_longlong
+        self._f("op_count_estimate").restype = C.c_longlong
 
     def _f(self, name):
-        return self.lib[self.pfx + name]
+        return getattr(self.lib, self.pfx + name)
 
     def _check(self, code: int):
         if code != 0:

@@ -1,0 +1,226 @@
+// dense.cu -- the dense SKP grid operator y = sum_r (A_r (x) B_r (x) C_r) x on
+// FP64 DMMA tensor cores (config 5; kron_matvec_shuffle semantics,
+// kron.hpp:180-197, summed over terms as spkmv_sum does, parallel.hpp:193-196).
+//
+// sm_100a has no FP64 tcgen05 kind (ptxas rejects .kind::f64), so FP64 tensor
+// work is warp-level mma.sync m8n8k4 (SASS DMMA.8x8x4). Every mode product is
+// one GEMM of the form
+//     out[m][i] = sum_k in[k][m] * F[i][k]          (M x N, contraction K)
+// which contracts the SLOWEST axis of a lexicographic tensor and appends the
+// result as the FASTEST axis. Three such passes rotate the axes back to the
+// original order: [x][y][z] -A-> [y][z][x'] -B-> [z][x'][y'] -C-> [x'][y'][z'].
+// The last pass contracts over (term, z) at once (K = chunk * n2), so the
+// per-term partial sums accumulate in the DMMA registers.
+#include <algorithm>
+
+#include "internal.h"
+
+namespace kb {
+namespace {
+
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, THREADS = 128;
+constexpr int LDA = BM + 8;  // As[k][m]: row offsets alternate 0/64 B mod 128 -> no conflicts
+constexpr int LDB = BK + 4;  // Bs[i][k]: row offsets step 32 B mod 128 -> no conflicts
+constexpr size_t kSmem = sizeof(double) * STAGES * (BK * LDA + BN * LDB);
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const int n = valid ? 8 : 0;  // zero-fill out-of-range elements
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, int valid_doubles) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const int n = valid_doubles * 8;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// VEC16: all rows 16-byte aligned (M and K even, pointers aligned) -> 16-byte copies.
+template <bool VEC16>
+__global__ void __launch_bounds__(THREADS) k_dgemm_tn(int64_t M, int64_t N, int64_t K,
+                                                      const double* __restrict__ in,
+                                                      const double* __restrict__ F,
+                                                      double* __restrict__ out, int accumulate) {
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;                         // [STAGES][BK][LDA]
+    double* Bs = smem + STAGES * BK * LDA;     // [STAGES][BN][LDB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;   // 2 x 2 warps, warp tile 64 x 32
+    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    const int ktiles = (int)((K + BK - 1) / BK);
+
+    auto load = [&](int stage, int kt) {
+        double* as = As + stage * BK * LDA;
+        double* bs = Bs + stage * BN * LDB;
+        const int64_t k0 = (int64_t)kt * BK;
+        if (VEC16) {
+            for (int idx = tid; idx < BK * BM / 2; idx += THREADS) {
+                const int kk = idx / (BM / 2), mm = (idx % (BM / 2)) * 2;
+                const int64_t gk = k0 + kk, gm = m0 + mm;
+                int v = (gk < K) ? (int)std::min<int64_t>(2, std::max<int64_t>(0, M - gm)) : 0;
+                const double* src = in + (v ? gk * M + gm : 0);
+                cp_async16(as + kk * LDA + mm, src, v);
+            }
+            for (int idx = tid; idx < BN * BK / 2; idx += THREADS) {
+                const int ii = idx / (BK / 2), kk = (idx % (BK / 2)) * 2;
+                const int64_t gi = n0 + ii, gk = k0 + kk;
+                int v = (gi < N) ? (int)std::min<int64_t>(2, std::max<int64_t>(0, K - gk)) : 0;
+                const double* src = F + (v ? gi * K + gk : 0);
+                cp_async16(bs + ii * LDB + kk, src, v);
+            }
+        } else {
+            for (int idx = tid; idx < BK * BM; idx += THREADS) {
+                const int kk = idx / BM, mm = idx % BM;
+                const int64_t gk = k0 + kk, gm = m0 + mm;
+                const bool v = gk < K && gm < M;
+                cp_async8(as + kk * LDA + mm, in + (v ? gk * M + gm : 0), v);
+            }
+            for (int idx = tid; idx < BN * BK; idx += THREADS) {
+                const int ii = idx / BK, kk = idx % BK;
+                const int64_t gi = n0 + ii, gk = k0 + kk;
+                const bool v = gi < N && gk < K;
+                cp_async8(bs + ii * LDB + kk, F + (v ? gi * K + gk : 0), v);
+            }
+        }
+    };
+
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ktiles) load(s, s);
+        cp_commit();
+    }
+    for (int kt = 0; kt < ktiles; ++kt) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        const int nk = kt + STAGES - 1;
+        if (nk < ktiles) load(nk % STAGES, nk);
+        cp_commit();
+        const double* as = As + (kt % STAGES) * BK * LDA + wm * 64 + (lane >> 2);
+        const double* bs = Bs + (kt % STAGES) * BN * LDB + (wn * 32 + (lane >> 2)) * LDB;
+#pragma unroll
+        for (int k4 = 0; k4 < BK; k4 += 4) {
+            double a[8], b[4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = as[(k4 + (lane & 3)) * LDA + i * 8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = bs[j * 8 * LDB + k4 + (lane & 3)];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+        }
+    }
+    cp_wait<0>();
+
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t row = m0 + wm * 64 + i * 8 + (lane >> 2);
+        if (row >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t col = n0 + wn * 32 + j * 8 + 2 * (lane & 3);
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+                if (col + c < N) {
+                    double* o = out + row * N + col + c;
+                    *o = accumulate ? *o + acc[i][j][c] : acc[i][j][c];
+                }
+        }
+    }
+}
+
+// Ccat[z'][r * n2 + z] = C_r[z'][z]: the term-concatenated last-pass operand.
+__global__ void k_concat_terms(int nterms, int n, const double* __restrict__ C,
+                               double* __restrict__ Ccat) {
+    const int64_t total = (int64_t)nterms * n * n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int z = (int)(e % n), zp = (int)((e / n) % n), r = (int)(e / ((int64_t)n * n));
+        Ccat[(int64_t)zp * nterms * n + (int64_t)r * n + z] = C[e];
+    }
+}
+
+int chunk_terms(int n0, int n1, int n2, int nterms) {
+    // keep the term-stacked intermediates within ~16 GB of HBM
+    const double mesh = 8.0 * n0 * n1 * n2;
+    int c = (int)std::max(1.0, std::min((double)nterms, 16e9 / mesh));
+    return std::max(1, std::min(c, nterms));
+}
+
+}  // namespace
+
+void dgemm_tn(cudaStream_t s, int64_t M, int64_t N, int64_t K, const double* in, const double* F,
+              double* out, bool accumulate) {
+    static bool attr = false;
+    if (!attr) {
+        KB_CUDA(cudaFuncSetAttribute(k_dgemm_tn<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSmem));
+        KB_CUDA(cudaFuncSetAttribute(k_dgemm_tn<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+        attr = true;
+    }
+    if (M <= 0 || N <= 0) return;
+    const dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
+    const bool vec = (M % 2 == 0) && (K % 2 == 0) && ((uintptr_t)in % 16 == 0) &&
+                     ((uintptr_t)F % 16 == 0);
+    if (vec)
+        k_dgemm_tn<true><<<grid, THREADS, kSmem, s>>>(M, N, K, in, F, out, accumulate ? 1 : 0);
+    else
+        k_dgemm_tn<false><<<grid, THREADS, kSmem, s>>>(M, N, K, in, F, out, accumulate ? 1 : 0);
+    KB_CHECK_LAUNCH();
+}
+
+size_t dense_workspace_bytes(int n0, int n1, int n2, int nterms) {
+    const size_t mesh = (size_t)n0 * n1 * n2;
+    const int c = chunk_terms(n0, n1, n2, nterms);
+    return sizeof(double) * (mesh * (1 + (size_t)c) + (size_t)n2 * n2 * c) + 256;
+}
+
+void kron_matvec_dense(cudaStream_t s, int n0, int n1, int n2, int nterms, const double* A,
+                       const double* B, const double* C, const double* x, double* y, double* work,
+                       size_t work_bytes) {
+    const int64_t mesh = (int64_t)n0 * n1 * n2;
+    if (nterms <= 0) {
+        KB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * mesh, s));
+        return;
+    }
+    const int chunk = chunk_terms(n0, n1, n2, nterms);
+    if (work_bytes < dense_workspace_bytes(n0, n1, n2, nterms))
+        throw Error(KPME_GPU_INVALID_ARGUMENT, "kron_matvec_dense: workspace too small");
+    double* t1 = work;                          // [n1][n2][n0]
+    double* t2 = t1 + mesh;                     // [chunk][n2][n0][n1]
+    double* ccat = t2 + mesh * chunk;           // [n2][chunk * n2]
+    for (int r0 = 0; r0 < nterms; r0 += chunk) {
+        const int cr = std::min(chunk, nterms - r0);
+        for (int r = 0; r < cr; ++r) {
+            const int t = r0 + r;
+            // pass A: contract x (K = n0): t1[(y,z)][x'] = sum_x x[x][(y,z)] A_t[x'][x]
+            dgemm_tn(s, (int64_t)n1 * n2, n0, n0, x, A + (int64_t)t * n0 * n0, t1, false);
+            // pass B: contract y (K = n1): t2_r[(z,x')][y'] = sum_y t1[y][(z,x')] B_t[y'][y]
+            dgemm_tn(s, (int64_t)n2 * n0, n1, n1, t1, B + (int64_t)t * n1 * n1, t2 + r * mesh,
+                     false);
+        }
+        // pass C over (term, z): y[(x',y')][z'] (+)= sum_{r,z} t2[r][z][(x',y')] C_r[z'][z]
+        k_concat_terms<<<148 * 4, 256, 0, s>>>(cr, n2, C + (int64_t)r0 * n2 * n2, ccat);
+        KB_CHECK_LAUNCH();
+        dgemm_tn(s, (int64_t)n0 * n1, n2, (int64_t)cr * n2, t2, ccat, y, r0 > 0);
+    }
+}
+
+}  // namespace kb

@@ -1,0 +1,111 @@
+// internal.h -- shared declarations of the sm_100a implementation behind
+// include/kpme_gpu.h. Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "kpme_gpu.h"
+
+namespace kb {
+
+// Status-carrying exception used inside the library; the C-ABI layer maps it
+// to a return code + kpme_gpu_last_error().
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define KB_CUDA(call)                                                               \
+    do {                                                                            \
+        cudaError_t e_ = (call);                                                    \
+        if (e_ != cudaSuccess)                                                      \
+            throw ::kb::Error(KPME_GPU_CUDA, std::string(#call) + ": " +            \
+                                                 cudaGetErrorString(e_));           \
+    } while (0)
+
+#define KB_CHECK_LAUNCH() KB_CUDA(cudaGetLastError())
+
+// Cell-grid geometry in the reference's terms (CellGrid, geometry.hpp:63-111)
+// plus the derived sizes the kernels need. Passed to kernels by value.
+struct Geometry {
+    double center[3];
+    double radius;
+    int K[3];      // cells per axis
+    int L;         // interpolation order (nodes per cell axis)
+    int n[3];      // mesh points per axis, K_a * L (cell-face nodes duplicated)
+    int M;         // modes
+    int R;         // compacted Fourier rows per axis, 2M+1 (the m=0 sine row is 0)
+    int ncell;     // K0*K1*K2
+    int z_lo, z_hi;  // cell planes along axis 2 owned by this plan (slab)
+};
+
+// ---- sort.cu ----------------------------------------------------------------
+struct SortBuffers {
+    int32_t* cnt;         // [ncell] histogram, then cursor
+    int32_t* start;       // [ncell+1]
+    int32_t* key;         // [n]
+    int32_t* perm;        // [n]
+    int32_t* big;         // [ncell] cells too large for the warp sorter
+    int32_t* nbig;        // [1]
+    unsigned long long* bad;  // [2]: lowest out-of-box index, out-of-cell flag
+};
+void launch_sort(const Geometry& g, int64_t n, const double* xyz, const SortBuffers& b,
+                 cudaStream_t s, int* launches);
+void launch_permute(int64_t n, const double* xyz, const double* q, const int32_t* perm,
+                    double4* sp, cudaStream_t s);
+
+// ---- interp.cu --------------------------------------------------------------
+// spread (+ forward z-contraction) per column of cells
+struct ColumnArgs {
+    Geometry g;
+    const int32_t* start;
+    const double4* sp;       // sorted particles (x, y, z, q)
+    const double* W2;        // [R][n2]
+    int S;                   // z segments per column
+    double* T1;              // [S][n0][n1][R]
+    double* colq;            // [S][K0*K1]
+    double* phi_cells;       // optional out / in
+    const double* B2;        // [n0][n1][R]
+    double* psi_cells;       // optional out / in
+    const double* corr;      // device scalar: c_Lambda * sum q (nullable)
+    const int32_t* perm;     // sorted slot -> particle index
+    double* out;             // potentials in particle order
+    unsigned long long* bad;
+};
+enum SpreadMode { SPREAD_PARTICLES = 0, SPREAD_FROM_CELLS = 1 };
+enum GatherMode { GATHER_FROM_B2 = 0, GATHER_FROM_CELLS = 1, PSI_ONLY = 2 };
+void launch_spread_fwd(const ColumnArgs& a, int mode, bool want_fwd, cudaStream_t s);
+void launch_bwd_gather(const ColumnArgs& a, int mode, cudaStream_t s);
+
+// ---- core.cu ----------------------------------------------------------------
+void launch_factor_tables(const Geometry& g, int nterms, const double* term_weights,
+                          const double* profiles, double* W0, double* W1, double* W2,
+                          double* D, double* G, cudaStream_t s);
+void launch_core_forward(const Geometry& g, int S, const double* T1, const double* W0,
+                         const double* W1, double* T2, const double* colq, double* F,
+                         cudaStream_t s);
+void launch_core_backward(const Geometry& g, const double* G, const double* F,
+                          double correction, const double* W0, const double* W1, double* B2,
+                          double* corr_out, cudaStream_t s);
+// corr = correction * sum(colq), columns in order
+void launch_charge_correction(const Geometry& g, int S, const double* colq, double correction,
+                              double* corr, cudaStream_t s);
+void launch_axis_operands(const Geometry& g, int axis, int nterms, const double* W,
+                          const double* D, double* out, cudaStream_t s);
+// inverse == false: src = cells, dst = mesh; inverse == true: src = mesh, dst = cells
+void launch_cells_to_mesh(const Geometry& g, const double* src, double* dst, bool inverse,
+                          cudaStream_t s);
+
+// ---- dense.cu ---------------------------------------------------------------
+void dgemm_tn(cudaStream_t s, int64_t M, int64_t N, int64_t K, const double* in,
+              const double* F, double* out, bool accumulate);
+size_t dense_workspace_bytes(int n0, int n1, int n2, int nterms);
+void kron_matvec_dense(cudaStream_t s, int n0, int n1, int n2, int nterms, const double* A,
+                       const double* B, const double* C, const double* x, double* y,
+                       double* work, size_t work_bytes);
+
+}  // namespace kb

@@ -1,0 +1,185 @@
+"""Steady-state plan API over torch device tensors (kpme_gpu_plan_*).
+
+torch supplies device memory and the stream; every kernel is ours
+(libkpme_b200.so). The plan runs on torch's current CUDA stream so it orders
+with surrounding torch work.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .api import CellGrid, EwaldConfig, KpmeOptions, SkpDecomposition, make_config
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda or t.dtype != torch.float64 and t.dtype != torch.int32:
+        raise ValueError("kpme_gpu: expected a CUDA float64/int32 tensor")
+    if not t.is_contiguous():
+        raise ValueError("kpme_gpu: expected a contiguous tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+class KpmePlan:
+    """Plan for repeated kpme_apply calls on one cell grid and decomposition."""
+
+    def __init__(self, cfg: EwaldConfig, grid: CellGrid, order: int, dec: SkpDecomposition,
+                 max_particles: int, opt: KpmeOptions | None = None, device: int = 0,
+                 formulation: str = "auto"):
+        if dec.modes != cfg.modes:
+            raise ValueError("kpme_apply: decomposition mode bound mismatch")
+        self.cfg, self.grid, self.order, self.dec = cfg, grid, order, dec
+        self.device = device
+        self.max_particles = int(max_particles)
+        self._c, self._keep = make_config(cfg, grid, order, dec, opt, device, formulation)
+        self._h = C.c_void_p()
+        with torch.cuda.device(device):
+            check(lib.kpme_gpu_plan_create(C.byref(self._c), self.max_particles,
+                                           C.byref(self._h)))
+        self.bind_stream()
+
+    def close(self):
+        if self._h:
+            lib.kpme_gpu_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def ncell(self) -> int:
+        return self.grid.cell_count()
+
+    @property
+    def grid_size(self) -> int:
+        return self.order ** 3
+
+    def bind_stream(self, stream: torch.cuda.Stream | None = None):
+        s = stream or torch.cuda.current_stream(self.device)
+        check(lib.kpme_gpu_plan_set_stream(self._h, C.c_void_p(s.cuda_stream)))
+
+    # ---- full pipeline --------------------------------------------------
+    def execute(self, xyz: torch.Tensor, q: torch.Tensor, out: torch.Tensor | None = None,
+                defer_checks: bool = False) -> torch.Tensor:
+        n = xyz.shape[0]
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=xyz.device)
+        flags = _lib.DEFER_CHECKS if defer_checks else 0
+        check(lib.kpme_gpu_plan_execute_device(self._h, n, _ptr(xyz), _ptr(q), _ptr(out), flags))
+        return out
+
+    def execute_graph(self, xyz: torch.Tensor, q: torch.Tensor, out: torch.Tensor):
+        check(lib.kpme_gpu_plan_graph_execute(self._h, xyz.shape[0], _ptr(xyz), _ptr(q),
+                                              _ptr(out)))
+        return out
+
+    def execute_host(self, xyz: np.ndarray, q: np.ndarray, out: np.ndarray | None = None):
+        """Host buffers (pinned or pageable); H2D/D2H inside the call."""
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        n = xyz.shape[0]
+        if out is None:
+            out = np.zeros(max(n, 1))
+        dp = C.POINTER(C.c_double)
+        check(lib.kpme_gpu_plan_execute(self._h, n, xyz.ctypes.data_as(dp), q.ctypes.data_as(dp),
+                                        out.ctypes.data_as(dp)))
+        return out[:n]
+
+    def execute_host_ptr(self, n: int, xyz_ptr: int, q_ptr: int, out_ptr: int):
+        """Host-pointer variant for pinned torch CPU tensors."""
+        dp = C.POINTER(C.c_double)
+        check(lib.kpme_gpu_plan_execute(self._h, n, C.cast(xyz_ptr, dp), C.cast(q_ptr, dp),
+                                        C.cast(out_ptr, dp)))
+
+    def status(self):
+        check(lib.kpme_gpu_plan_status(self._h))
+
+    def launches(self) -> int:
+        return lib.kpme_gpu_plan_launches(self._h)
+
+    def enable_timing(self, on: bool = True):
+        check(lib.kpme_gpu_plan_enable_timing(self._h, int(on)))
+
+    def stage_times(self):
+        buf = (C.c_double * 16)()
+        cnt = C.c_int()
+        check(lib.kpme_gpu_plan_stage_times(self._h, buf, 16, C.byref(cnt)))
+        return list(buf[: cnt.value])
+
+    # ---- stages ---------------------------------------------------------
+    def sort(self, xyz: torch.Tensor):
+        """assign_particles (geometry.hpp:131-154): (perm, cell_start)."""
+        n = xyz.shape[0]
+        perm = torch.empty(max(n, 1), dtype=torch.int32, device=xyz.device)
+        start = torch.empty(self.ncell + 1, dtype=torch.int32, device=xyz.device)
+        check(lib.kpme_gpu_sort(self._h, n, _ptr(xyz), _ptr(perm), _ptr(start)))
+        return perm[:n], start
+
+    def spread(self, xyz: torch.Tensor, q: torch.Tensor) -> torch.Tensor:
+        """InterpOperator::interpolate (interpolation.hpp:84-92): [ncell, L^3]."""
+        phi = torch.empty(self.ncell, self.grid_size, dtype=torch.float64, device=xyz.device)
+        check(lib.kpme_gpu_spread(self._h, xyz.shape[0], _ptr(xyz), _ptr(q), _ptr(phi)))
+        return phi
+
+    def skp_apply(self, phi: torch.Tensor) -> torch.Tensor:
+        """spkmv_sum over all terms (parallel.hpp:184-228)."""
+        psi = torch.empty_like(phi)
+        check(lib.kpme_gpu_skp_apply(self._h, _ptr(phi.contiguous()), _ptr(psi)))
+        return psi
+
+    def gather(self, xyz: torch.Tensor, psi: torch.Tensor) -> torch.Tensor:
+        """InterpOperator::anterpolate (interpolation.hpp:95-105)."""
+        out = torch.empty(xyz.shape[0], dtype=torch.float64, device=xyz.device)
+        check(lib.kpme_gpu_gather(self._h, xyz.shape[0], _ptr(xyz), _ptr(psi.contiguous()),
+                                  _ptr(out)))
+        return out
+
+    def axis_operands(self, axis: int) -> torch.Tensor:
+        """Dense A_a(lambda) = W_a^T diag(d) W_a for every term: [nterms, n_a, n_a]."""
+        n = self.grid.counts[axis] * self.order
+        out = torch.empty(max(len(self.dec.terms), 1), n, n, dtype=torch.float64,
+                          device=f"cuda:{self.device}")
+        check(lib.kpme_gpu_plan_axis_operands(self._h, axis, _ptr(out)))
+        return out[: len(self.dec.terms)]
+
+
+def kron_matvec_dense(A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, x: torch.Tensor,
+                      out: torch.Tensor | None = None, workspace: torch.Tensor | None = None):
+    """y = sum_r (A_r (x) B_r (x) C_r) x on the lexicographic mesh x[n0, n1, n2]
+    (kron_matvec_shuffle, kron.hpp:180-197, summed over terms) on FP64 DMMA."""
+    nt, n0, _ = A.shape
+    n1, n2 = B.shape[1], C_.shape[1]
+    if out is None:
+        out = torch.empty(n0, n1, n2, dtype=torch.float64, device=x.device)
+    ws, wsb = None, 0
+    if workspace is not None:
+        ws, wsb = _ptr(workspace), workspace.numel() * workspace.element_size()
+    s = torch.cuda.current_stream(x.device)
+    check(lib.kpme_gpu_kron_matvec_dense(x.device.index or 0, C.c_void_p(s.cuda_stream), n0, n1,
+                                         n2, nt, _ptr(A.contiguous()), _ptr(B.contiguous()),
+                                         _ptr(C_.contiguous()), _ptr(x.contiguous()), _ptr(out),
+                                         ws, wsb))
+    return out
+
+
+def dense_workspace_bytes(n0: int, n1: int, n2: int, nterms: int) -> int:
+    return int(lib.kpme_gpu_dense_workspace_bytes(n0, n1, n2, nterms))
+
+
+def dgemm_tn(inp: torch.Tensor, F: torch.Tensor, out: torch.Tensor, accumulate=False):
+    """out[m][i] (+)= sum_k inp[k][m] F[i][k] on the DMMA GEMM kernel."""
+    K, M = inp.shape
+    N = F.shape[0]
+    s = torch.cuda.current_stream(inp.device)
+    check(lib.kpme_gpu_dgemm_tn(C.c_void_p(s.cuda_stream), M, N, K, _ptr(inp), _ptr(F),
+                                _ptr(out), int(accumulate)))
+    return out

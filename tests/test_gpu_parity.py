@@ -1,0 +1,346 @@
+"""GPU parity: the sm_100a path through the C ABI against the CPU oracle and
+the reference's golden vectors. Tolerances: bit-exact for the cell sort
+(north star), 1e-13 / 1e-12 for the interpolation stages and the SKP apply
+(the reference's own test tolerances, test_interpolation.cpp:120-168,
+test_parallel.cpp:132-234), 1e-10 relative L2 end to end (north star)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+UNIT = ((0.5, 0.5, 0.5), 0.5)
+E2E_TOL = 1e-10
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    den = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (den if den > 0 else 1.0)
+
+
+def fnv1a64(a):
+    h = 0xCBF29CE484222325
+    for b in np.ascontiguousarray(a, dtype="<i4").tobytes():
+        h ^= b
+        h = (h * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def kp_objects(pb):
+    """Reference-API objects for an oracle Problem."""
+    import paper_2601_18838_b200 as kp
+
+    cfg = kp.EwaldConfig(pb.xi, pb.modes)
+    grid = kp.build_cell_grid(kp.Box3(pb.center, pb.radius), pb.counts)
+    dec = kp.SkpDecomposition(kp.SkpKind.sinc, pb.modes if pb.dec_modes is None else pb.dec_modes,
+                              pb.correction,
+                              [kp.SkpTerm(float(w), tuple(np.array(p) for p in prof))
+                               for w, prof in zip(pb.term_weights, pb.profiles)])
+    return cfg, grid, dec, kp.PointCloud(np.asarray(pb.pos)), kp.ChargeVector(np.asarray(pb.q))
+
+
+def plan_for(pb, formulation="auto", n=None):
+    from paper_2601_18838_b200.plan import KpmePlan
+
+    cfg, grid, dec, cloud, q = kp_objects(pb)
+    return KpmePlan(cfg, grid, pb.order, dec, len(pb.q) if n is None else n,
+                    formulation=formulation)
+
+
+def dev(x, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device="cuda")
+
+
+def golden_problem(oracle, golden, name):
+    from oracle.binding import Problem
+    from tests.golden.gen_golden import SMALL
+
+    spec = SMALL[name]
+    rule = oracle.sinc_rule_for_eps(spec["eps"], spec["modes"])
+    tw, prof, corr = oracle.skp_from_quadrature(rule, spec["xi"], spec["modes"])
+    counts = spec["counts"]
+    counts = (counts,) * 3 if isinstance(counts, int) else tuple(counts)
+    return Problem(xi=spec["xi"], modes=spec["modes"], center=tuple(spec["center"]),
+                   radius=spec["radius"], counts=counts, order=spec["order"], term_weights=tw,
+                   profiles=prof, correction=corr, pos=golden[f"e2e_{name}_pos"],
+                   q=golden[f"e2e_{name}_q"])
+
+
+# ---- cell sort: bit-exact --------------------------------------------------
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_sort_bit_exact_kat(oracle, golden, name):
+    from oracle.binding import make_problem
+
+    n, k, h_hi, h_lo, s_hi, s_lo = (int(v) for v in golden[f"sort_{name}_meta"])
+    pb = make_problem(oracle, n=n, counts=k, order=4, eps=1e-6)
+    plan = plan_for(pb)
+    perm, start = plan.sort(dev(pb.pos))
+    perm, start = perm.cpu().numpy(), start.cpu().numpy()
+    operm, ostart = oracle.assign_particles(*UNIT, (k, k, k), pb.pos)
+    np.testing.assert_array_equal(perm, operm)
+    np.testing.assert_array_equal(start, ostart)
+    assert fnv1a64(perm) == (h_hi << 32 | h_lo)
+    assert fnv1a64(start) == (s_hi << 32 | s_lo)
+
+
+def test_sort_edges_and_ties(oracle, golden):
+    from oracle.binding import make_problem
+
+    pb = make_problem(oracle, n=6, counts=(2, 3, 4), order=3, modes=2, eps=1e-6,
+                      center=(0, 0, 0), radius=1.0)
+    pb.pos = golden["sort_edge_pos"]
+    plan = plan_for(pb)
+    perm, start = plan.sort(dev(pb.pos))
+    np.testing.assert_array_equal(perm.cpu().numpy(), golden["sort_edge_perm"])
+    np.testing.assert_array_equal(start.cpu().numpy(), golden["sort_edge_start"])
+
+
+@pytest.mark.parametrize("n,counts", [(5000, (2, 1, 1)), (40000, (1, 1, 1)), (3000, (3, 5, 7))])
+def test_sort_large_cells(oracle, n, counts):
+    """Cells beyond the warp (1024) and CTA (16384) sorters."""
+    from oracle.binding import make_problem
+
+    pb = make_problem(oracle, n=n, counts=counts, order=3, modes=2, eps=1e-6, seed=9)
+    plan = plan_for(pb)
+    perm, start = plan.sort(dev(pb.pos))
+    operm, ostart = oracle.assign_particles(*UNIT, counts, pb.pos)
+    np.testing.assert_array_equal(perm.cpu().numpy(), operm)
+    np.testing.assert_array_equal(start.cpu().numpy(), ostart)
+
+
+def test_outside_particle_rejected_with_index(oracle):
+    from oracle.binding import make_problem
+
+    pb = make_problem(oracle, n=100, counts=4, order=4, modes=2, eps=1e-6)
+    pos = pb.pos.copy()
+    pos[37] = (1.5, 0.5, 0.5)
+    pos[80] = (0.5, -0.2, 0.5)
+    plan = plan_for(pb)
+    with pytest.raises(ValueError, match="particle 37 outside the box"):
+        plan.execute(dev(pos), dev(pb.q))
+    # the plan stays usable
+    z = plan.execute(dev(pb.pos), dev(pb.q)).cpu().numpy()
+    assert rel(z, oracle.kpme_apply(pb)) <= E2E_TOL
+
+
+# ---- stages ----------------------------------------------------------------
+
+def test_spread_matches_reference(oracle, golden):
+    pb = golden_problem(oracle, golden, "cfg1")
+    plan = plan_for(pb)
+    phi = plan.spread(dev(pb.pos), dev(pb.q)).cpu().numpy()
+    ref = golden["stage_cfg1_phi"]
+    assert rel(phi, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["rect", "sparse", "accept4_421"])
+def test_spread_gather_adjoint_and_oracle(oracle, golden, name):
+    pb = golden_problem(oracle, golden, name)
+    plan = plan_for(pb)
+    phi = plan.spread(dev(pb.pos), dev(pb.q)).cpu().numpy()
+    assert rel(phi, oracle.interpolate(pb)) <= 1e-13
+    rng = np.random.default_rng(1)
+    g = rng.uniform(-1, 1, phi.shape)
+    z = plan.gather(dev(pb.pos), dev(g)).cpu().numpy()
+    assert rel(z, oracle.anterpolate(pb, g)) <= 1e-13
+    # adjointness <S q, g> = <q, S^T g> (test_interpolation.cpp:170-193)
+    assert np.dot(phi.ravel(), g.ravel()) == pytest.approx(np.dot(pb.q, z), rel=1e-12)
+
+
+def test_skp_apply_matches_reference(oracle, golden):
+    pb = golden_problem(oracle, golden, "cfg1")
+    plan = plan_for(pb)
+    psi = plan.skp_apply(dev(golden["stage_cfg1_phi"])).cpu().numpy()
+    assert rel(psi, golden["stage_cfg1_psi"]) <= 1e-12
+    assert rel(psi, golden["stage_cfg1_psi_fused"]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["rect", "accept4_421"])
+def test_skp_apply_structured_vs_oracle(oracle, golden, name):
+    pb = golden_problem(oracle, golden, name)
+    plan = plan_for(pb)
+    rng = np.random.default_rng(2)
+    phi = rng.uniform(-1, 1, (int(np.prod(pb.counts)), pb.order ** 3))
+    psi = plan.skp_apply(dev(phi)).cpu().numpy()
+    assert rel(psi, oracle.spkmv_sum(pb, phi)) <= 1e-12
+    dplan = plan_for(pb, formulation="dense")
+    psi_d = dplan.skp_apply(dev(phi)).cpu().numpy()
+    assert rel(psi_d, psi) <= 1e-12
+
+
+# ---- end to end --------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["cfg1", "single_cell", "split_k1", "split_k2", "accept1",
+                                  "accept4_421", "rect", "sparse"])
+def test_e2e_vs_reference_golden(oracle, golden, name):
+    import paper_2601_18838_b200 as kp
+
+    pb = golden_problem(oracle, golden, name)
+    cfg, grid, dec, cloud, q = kp_objects(pb)
+    res = kp.kpme_apply(cfg, grid, pb.order, dec, cloud, q)
+    assert rel(res.potentials, golden[f"e2e_{name}_pot"]) <= E2E_TOL
+    assert rel(res.potentials, golden[f"e2e_{name}_pot_fused"]) <= E2E_TOL
+    assert len(res.ledger_array) == golden[f"e2e_{name}_ledger_rows"][0]
+    if f"e2e_{name}_dense" in golden:  # physics vs the brute-force oracle
+        tol = {"single_cell": 1e-4, "accept1": 1e-5}.get(name)
+        if tol:
+            assert rel(res.potentials, golden[f"e2e_{name}_dense"]) <= tol
+
+
+@pytest.mark.parametrize("name", ["cfg1", "accept4_421"])
+def test_e2e_dense_formulation(oracle, golden, name):
+    pb = golden_problem(oracle, golden, name)
+    plan = plan_for(pb, formulation="dense")
+    z = plan.execute(dev(pb.pos), dev(pb.q)).cpu().numpy()
+    assert rel(z, golden[f"e2e_{name}_pot"]) <= E2E_TOL
+
+
+def test_e2e_cfg2_vs_oracle_and_golden(oracle, golden):
+    from paper_2601_18838_b200 import inputs
+
+    w = inputs.workload("cfg2")
+    from paper_2601_18838_b200.plan import KpmePlan
+
+    plan = KpmePlan(w.cfg, w.grid, w.order, w.dec, w.n)
+    z = plan.execute(dev(w.data.cloud.positions), dev(w.data.charges.values)).cpu().numpy()
+    idx = golden["e2e_cfg2_idx"]
+    assert rel(z[idx], golden["e2e_cfg2_pot_sample"]) <= E2E_TOL
+    assert abs(np.linalg.norm(z) - golden["e2e_cfg2_norms"][0]) <= E2E_TOL * golden["e2e_cfg2_norms"][0]
+    tw, prof = w.dec.arrays()
+    from oracle.binding import Problem
+
+    pb = Problem(xi=w.cfg.xi, modes=w.cfg.modes, center=w.grid.box.center,
+                 radius=w.grid.box.radius, counts=w.grid.counts, order=w.order, term_weights=tw,
+                 profiles=prof, correction=w.dec.correction, pos=w.data.cloud.positions,
+                 q=w.data.charges.values)
+    ref = oracle.kpme_apply(pb, threads=os.cpu_count() or 1)
+    assert rel(z, ref) <= E2E_TOL
+
+
+def test_e2e_cfg3_vs_oracle(oracle):
+    from oracle.binding import Problem
+    from paper_2601_18838_b200 import inputs
+    from paper_2601_18838_b200.plan import KpmePlan
+
+    w = inputs.workload("cfg3")
+    plan = KpmePlan(w.cfg, w.grid, w.order, w.dec, w.n)
+    z = plan.execute(dev(w.data.cloud.positions), dev(w.data.charges.values)).cpu().numpy()
+    tw, prof = w.dec.arrays()
+    pb = Problem(xi=w.cfg.xi, modes=w.cfg.modes, center=w.grid.box.center,
+                 radius=w.grid.box.radius, counts=w.grid.counts, order=w.order, term_weights=tw,
+                 profiles=prof, correction=w.dec.correction, pos=w.data.cloud.positions,
+                 q=w.data.charges.values)
+    ref = oracle.kpme_apply(pb, fuse_terms=False, threads=os.cpu_count() or 1)
+    assert rel(z, ref) <= E2E_TOL
+
+
+def test_e2e_cfg4_properties():
+    """Config 4 (3M sites) at full size: size-independent properties --
+    symmetry <q1, H q2> = <q2, H q1> of the SPD-like operator S^T H S - c 11^T,
+    linearity, and bit-identical re-runs."""
+    from paper_2601_18838_b200 import inputs
+    from paper_2601_18838_b200.plan import KpmePlan
+
+    w = inputs.workload("cfg4")
+    plan = KpmePlan(w.cfg, w.grid, w.order, w.dec, w.n)
+    xyz = dev(w.data.cloud.positions)
+    q1 = dev(w.data.charges.values)
+    q2 = dev(np.random.default_rng(4).uniform(-1, 1, w.n))
+    z1 = plan.execute(xyz, q1).clone()
+    z2 = plan.execute(xyz, q2).clone()
+    a, b = float(torch.dot(q2, z1)), float(torch.dot(q1, z2))
+    scale = float(torch.linalg.norm(q2) * torch.linalg.norm(z1))
+    assert abs(a - b) <= 1e-12 * scale
+    z12 = plan.execute(xyz, 2.0 * q1 - 0.5 * q2)
+    assert float(torch.linalg.norm(z12 - (2.0 * z1 - 0.5 * z2))) <= 1e-12 * float(torch.linalg.norm(z12))
+    z1b = plan.execute(xyz, q1)
+    assert torch.equal(z1, z1b)
+
+
+def test_determinism_and_graph(oracle, golden):
+    pb = golden_problem(oracle, golden, "sparse")
+    plan = plan_for(pb)
+    xyz, q = dev(pb.pos), dev(pb.q)
+    a = plan.execute(xyz, q).clone()
+    b = plan.execute(xyz, q).clone()
+    assert torch.equal(a, b)
+    out = torch.empty_like(a)
+    plan.execute_graph(xyz, q, out)
+    plan.execute_graph(xyz, q, out)
+    torch.cuda.synchronize()
+    assert torch.equal(a, out)
+    h = plan.execute_host(pb.pos, pb.q)
+    assert np.array_equal(h, a.cpu().numpy())
+
+
+def test_zero_charges_empty_cloud_and_no_terms(oracle):
+    import paper_2601_18838_b200 as kp
+    from oracle.binding import make_problem
+
+    pb = make_problem(oracle, n=32, counts=2, order=4, modes=2, eps=1e-6, center=(0, 0, 0),
+                      radius=0.02, seed=5)
+    cfg, grid, dec, cloud, q = kp_objects(pb)
+    z = kp.kpme_apply(cfg, grid, 4, dec, cloud, kp.ChargeVector(np.zeros(32))).potentials
+    assert (z == 0.0).all()
+    empty = kp.kpme_apply(cfg, grid, 4, dec, kp.PointCloud(np.zeros((0, 3))),
+                          kp.ChargeVector(np.zeros(0)))
+    assert empty.potentials.shape == (0,)
+    none = kp.kpme_apply(cfg, grid, 4, dec.truncated(0), cloud, q)
+    np.testing.assert_allclose(none.potentials, -dec.correction * q.values.sum(), rtol=1e-14)
+    bad = kp.SkpDecomposition(dec.kind, 3, dec.correction, dec.terms)
+    with pytest.raises(ValueError, match="mode bound mismatch"):
+        kp.kpme_apply(cfg, grid, 4, bad, cloud, q)
+
+
+# ---- dense operator (config 5 semantics) -----------------------------------
+
+@pytest.mark.parametrize("n", [6, 16])
+def test_dense_kron_matvec_matches_reference(golden, n):
+    from paper_2601_18838_b200.plan import kron_matvec_dense
+
+    f = golden[f"kron_n{n}_factors"]
+    A, B, C_ = (dev(f[i][None]) for i in range(3))
+    x = dev(golden[f"kron_n{n}_q"]).reshape(n, n, n)
+    y = kron_matvec_dense(A, B, C_, x).cpu().numpy().ravel()
+    assert rel(y, golden[f"kron_n{n}_out"]) <= 1e-13
+
+
+def test_dense_multi_term_vs_oracle_and_collapsed(oracle):
+    """Config-5 construction at n = 32 (K=4, L=8), R = 8 terms: DMMA dense
+    operator vs the oracle's per-term shuffle and vs the collapsed form."""
+    from paper_2601_18838_b200 import inputs
+    from paper_2601_18838_b200.plan import KpmePlan, kron_matvec_dense
+
+    cfg, grid, L, dec = inputs.dense_case(32, 8)
+    plan = KpmePlan(cfg, grid, L, dec, 1)
+    ops = [plan.axis_operands(a) for a in range(3)]
+    x = torch.randn(32, 32, 32, dtype=torch.float64, device="cuda",
+                    generator=torch.Generator(device="cuda").manual_seed(0))
+    y = kron_matvec_dense(*ops, x).cpu().numpy().ravel()
+    xs = x.cpu().numpy().ravel()
+    ref = np.zeros_like(xs)
+    for t in range(8):
+        out, mult = oracle.kron_matvec_shuffle([ops[a][t].cpu().numpy() for a in range(3)], xs)
+        ref += out
+        assert mult == 3 * 32 ** 4
+    assert rel(y, ref) <= 1e-12
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 64, 64), (300, 70, 37), (4096, 128, 512), (17, 5, 3)])
+def test_dgemm_tn(M, N, K):
+    from paper_2601_18838_b200.plan import dgemm_tn
+
+    g = torch.Generator(device="cuda").manual_seed(1)
+    a = torch.randn(K, M, dtype=torch.float64, device="cuda", generator=g)
+    f = torch.randn(N, K, dtype=torch.float64, device="cuda", generator=g)
+    out = torch.zeros(M, N, dtype=torch.float64, device="cuda")
+    dgemm_tn(a, f, out)
+    ref = a.T @ f.T
+    assert float(torch.linalg.norm(out - ref) / torch.linalg.norm(ref)) <= 1e-14
+    dgemm_tn(a, f, out, accumulate=True)
+    assert float(torch.linalg.norm(out - 2 * ref) / torch.linalg.norm(ref)) <= 1e-14

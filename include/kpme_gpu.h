@@ -122,7 +122,9 @@ int kpme_gpu_apply(const kpme_gpu_config* cfg, int64_t n, const double* xyz,
 int kpme_gpu_plan_create(const kpme_gpu_config* cfg, int64_t max_particles,
                          kpme_gpu_plan* out);
 int kpme_gpu_plan_destroy(kpme_gpu_plan plan);
-/* The plan runs on this stream (cudaStream_t as void*; NULL = its own). */
+/* The plan runs on this stream from now on (cudaStream_t as void*; NULL =
+ * the legacy default stream, which cannot be graph-captured). A new plan
+ * owns a non-blocking stream. */
 int kpme_gpu_plan_set_stream(kpme_gpu_plan plan, void* stream);
 /* Host buffers; H2D of xyz/q and D2H of potentials happen inside. */
 int kpme_gpu_plan_execute(kpme_gpu_plan plan, int64_t n, const double* xyz,

@@ -70,41 +70,66 @@ __global__ void k_factor_g(Geometry g, int nterms, const double* __restrict__ D,
     }
 }
 
+// Deterministic block sum of v[0..n): fixed per-thread strides, fixed tree.
+__device__ double block_sum(const double* __restrict__ v, int n, double* red) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    return red[0];
+}
+
 // T2[x][r1][r2] = sum_y W1[r1][y] * sum_seg T1[seg][x][y][r2]
+// All operands staged in shared memory first (coalesced, loads in flight).
 __global__ void k_core_a(Geometry g, int S, const double* __restrict__ T1,
                          const double* __restrict__ W1, double* __restrict__ T2) {
-    extern __shared__ double t1x[];  // n1 x R
+    extern __shared__ double sh[];
     const int x = blockIdx.x, n1 = g.n[1], R = g.R;
+    double* t1x = sh;             // n1 x R
+    double* w1 = sh + n1 * R;     // R x n1
     const int64_t seg_stride = (int64_t)g.n[0] * n1 * R;
     for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
         double s = 0.0;
         for (int seg = 0; seg < S; ++seg) s += T1[seg * seg_stride + (int64_t)x * n1 * R + e];
         t1x[e] = s;
+        w1[e] = W1[e];
     }
     __syncthreads();
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
         const int r1 = e / R, r2 = e % R;
         double s = 0.0;
-        for (int y = 0; y < n1; ++y) s = fma(W1[(int64_t)r1 * n1 + y], t1x[y * R + r2], s);
+        for (int y = 0; y < n1; ++y) s = fma(w1[r1 * n1 + y], t1x[y * R + r2], s);
         T2[(int64_t)x * R * R + e] = s;
     }
 }
 
-// F[r0][e] = sum_x W0[r0][x] T2[x][e]; F[R^3] = sum q (columns in order).
+// F[r0][e] = sum_x W0[r0][x] T2[x][e]; one CTA per (r0, e-chunk of 32):
+// each warp reduces a strided slice of x, warps combined in a fixed order.
+// F[R^3] = sum q (columns in order).
 __global__ void k_core_b(Geometry g, int S, const double* __restrict__ T2,
                          const double* __restrict__ W0, const double* __restrict__ colq,
                          double* __restrict__ F) {
-    const int r0 = blockIdx.x, R = g.R, n0 = g.n[0];
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-        double s = 0.0;
-        for (int x = 0; x < n0; ++x) s = fma(W0[(int64_t)r0 * n0 + x], T2[(int64_t)x * R * R + e], s);
-        F[(int64_t)r0 * R * R + e] = s;
+    __shared__ double part[8][32];
+    __shared__ double red[256];
+    const int R = g.R, RR = R * R, n0 = g.n[0];
+    const int r0 = blockIdx.x, e = blockIdx.y * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5;
+    double s = 0.0;
+    if (e < RR)
+        for (int x = w; x < n0; x += 8) s = fma(W0[(int64_t)r0 * n0 + x], T2[(int64_t)x * RR + e], s);
+    part[w][threadIdx.x & 31] = s;
+    __syncthreads();
+    if (w == 0 && e < RR) {
+        double t = 0.0;
+        for (int k = 0; k < 8; ++k) t += part[k][threadIdx.x];
+        F[(int64_t)r0 * RR + e] = t;
     }
-    if (r0 == 0 && threadIdx.x == 0) {
-        double q = 0.0;
-        const int ncol = g.K[0] * g.K[1];
-        for (int i = 0; i < S * ncol; ++i) q += colq[i];
-        F[R * R * R] = q;
+    if (r0 == 0 && blockIdx.y == 0) {
+        const double q = block_sum(colq, S * g.K[0] * g.K[1], red);
+        if (threadIdx.x == 0) F[R * RR] = q;
     }
 }
 
@@ -114,31 +139,36 @@ __global__ void k_core_c(Geometry g, const double* __restrict__ G, const double*
                          double correction, const double* __restrict__ W0,
                          const double* __restrict__ W1, double* __restrict__ B2,
                          double* __restrict__ corr) {
-    extern __shared__ double b1[];  // R x R
-    const int x = blockIdx.x, R = g.R, n0 = g.n[0], n1 = g.n[1];
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    extern __shared__ double sh[];
+    const int x = blockIdx.x, R = g.R, RR = R * R, n0 = g.n[0], n1 = g.n[1];
+    double* b1 = sh;            // R x R
+    double* w1 = sh + RR;       // R x n1
+    double* h = w1 + R * n1;    // R^3: G .* F
+    double* w0 = h + RR * R;    // R
+    for (int e = threadIdx.x; e < RR * R; e += blockDim.x) h[e] = G[e] * F[e];
+    for (int e = threadIdx.x; e < R * n1; e += blockDim.x) w1[e] = W1[e];
+    if (threadIdx.x < R) w0[threadIdx.x] = W0[(int64_t)threadIdx.x * n0 + x];
+    __syncthreads();
+    for (int e = threadIdx.x; e < RR; e += blockDim.x) {
         double s = 0.0;
-        for (int r0 = 0; r0 < R; ++r0)
-            s = fma(W0[(int64_t)r0 * n0 + x], G[r0 * R * R + e] * F[r0 * R * R + e], s);
+        for (int r0 = 0; r0 < R; ++r0) s = fma(w0[r0], h[r0 * RR + e], s);
         b1[e] = s;
     }
     __syncthreads();
     for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
         const int y = e / R, r2 = e % R;
         double s = 0.0;
-        for (int r1 = 0; r1 < R; ++r1) s = fma(W1[(int64_t)r1 * n1 + y], b1[r1 * R + r2], s);
+        for (int r1 = 0; r1 < R; ++r1) s = fma(w1[r1 * n1 + y], b1[r1 * R + r2], s);
         B2[(int64_t)x * n1 * R + e] = s;
     }
-    if (x == 0 && threadIdx.x == 0) *corr = correction * F[R * R * R];
+    if (x == 0 && threadIdx.x == 0) *corr = correction * F[R * RR];
 }
 
 __global__ void k_charge_correction(Geometry g, int S, const double* __restrict__ colq,
                                     double correction, double* __restrict__ corr) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double q = 0.0;
-        for (int i = 0; i < S * g.K[0] * g.K[1]; ++i) q += colq[i];
-        *corr = correction * q;
-    }
+    __shared__ double red[128];
+    const double q = block_sum(colq, S * g.K[0] * g.K[1], red);
+    if (threadIdx.x == 0) *corr = correction * q;
 }
 
 // out[t][u][v] = sum_r W[r][u] D[t][a][r] W[r][v]  (dense A_a(lambda))
@@ -193,23 +223,31 @@ void launch_factor_tables(const Geometry& g, int nterms, const double* tw, const
 void launch_core_forward(const Geometry& g, int S, const double* T1, const double* W0,
                          const double* W1, double* T2, const double* colq, double* F,
                          cudaStream_t s) {
-    k_core_a<<<g.n[0], 128, sizeof(double) * g.n[1] * g.R, s>>>(g, S, T1, W1, T2);
+    static bool attr = false;
+    if (!attr) {
+        KB_CUDA(cudaFuncSetAttribute(k_core_a, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+        KB_CUDA(cudaFuncSetAttribute(k_core_c, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+        attr = true;
+    }
+    k_core_a<<<g.n[0], 128, sizeof(double) * 2 * g.n[1] * g.R, s>>>(g, S, T1, W1, T2);
     KB_CHECK_LAUNCH();
-    k_core_b<<<g.R, 128, 0, s>>>(g, S, T2, W0, colq, F);
+    k_core_b<<<dim3(g.R, (g.R * g.R + 31) / 32), 256, 0, s>>>(g, S, T2, W0, colq, F);
     KB_CHECK_LAUNCH();
 }
 
 void launch_core_backward(const Geometry& g, const double* G, const double* F, double correction,
                           const double* W0, const double* W1, double* B2, double* corr,
                           cudaStream_t s) {
-    k_core_c<<<g.n[0], 128, sizeof(double) * g.R * g.R, s>>>(g, G, F, correction, W0, W1, B2,
-                                                             corr);
+    const size_t sh = sizeof(double) * ((size_t)g.R * g.R * (g.R + 1) + (size_t)g.R * g.n[1] + g.R);
+    k_core_c<<<g.n[0], 256, sh, s>>>(g, G, F, correction, W0, W1, B2, corr);
     KB_CHECK_LAUNCH();
 }
 
 void launch_charge_correction(const Geometry& g, int S, const double* colq, double correction,
                               double* corr, cudaStream_t s) {
-    k_charge_correction<<<1, 32, 0, s>>>(g, S, colq, correction, corr);
+    k_charge_correction<<<1, 128, 0, s>>>(g, S, colq, correction, corr);
     KB_CHECK_LAUNCH();
 }
 

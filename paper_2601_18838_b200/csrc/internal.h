@@ -48,6 +48,7 @@ struct SortBuffers {
     int32_t* cnt;         // [ncell] histogram, then cursor
     int32_t* start;       // [ncell+1]
     int32_t* key;         // [n]
+    int32_t* rank;        // [n] provisional slot within the cell
     int32_t* perm;        // [n]
     int32_t* big;         // [ncell] cells too large for the warp sorter
     int32_t* nbig;        // [1]

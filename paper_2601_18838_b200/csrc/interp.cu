@@ -259,6 +259,402 @@ __global__ void __launch_bounds__(kThreads) k_bwd_gather(ColumnArgs a, int cells
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Compile-time-L kernels (the hot path). Register arrays stay in registers.
+// ---------------------------------------------------------------------------
+
+template <int L>
+__device__ __forceinline__ void lagrange_t(const double* lc, double lo, double hi, double y,
+                                           double (&w)[L], unsigned long long* bad) {
+    const double slack = 1e-12 * (hi - lo);  // tensor_weights, interpolation.hpp:47-49
+    if (y < lo - slack || y > hi + slack) atomicOr(&bad[1], 1ull);
+    const double t = (y - 0.5 * (hi + lo)) / (0.5 * (hi - lo));
+    constexpr double step = 2.0 / (L - 1);
+    double pre = 1.0;
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+        w[k] = pre;
+        pre *= t - (-1.0 + step * k);
+    }
+    double suf = 1.0;
+#pragma unroll
+    for (int k = L - 1; k >= 0; --k) {
+        w[k] *= suf * lc[k];
+        suf *= t - (-1.0 + step * k);
+    }
+}
+
+__device__ __forceinline__ void lagrange_consts(int L, double* lc) {
+    const int k = threadIdx.x;
+    if (k < L) {
+        double d = 1.0;
+        for (int j = 0; j < L; ++j)
+            if (j != k) d *= (2.0 * k / (L - 1)) - (2.0 * j / (L - 1));
+        lc[k] = 1.0 / d;
+    }
+}
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+// c_k = 1 / prod_{j != k} (t_k - t_j) for equispaced t_j = -1 + 2j/(L-1),
+// evaluated at compile time.
+template <int L>
+struct LagrangeConsts {
+    double c[L];
+    constexpr LagrangeConsts() : c() {
+        for (int k = 0; k < L; ++k) {
+            double d = 1.0;
+            for (int j = 0; j < L; ++j)
+                if (j != k) d *= (2.0 * k / (L - 1)) - (2.0 * j / (L - 1));
+            c[k] = 1.0 / d;
+        }
+    }
+};
+
+// Division-free Lagrange weights: t = (y - mid) * inv_half with mid, inv_half
+// precomputed once per cell axis (same nodes as lagrange_weights_1d,
+// interpolation.hpp:20-36; rounding differs by a few ulps).
+template <int L>
+__device__ __forceinline__ void lagrange_fast(const double* /*lc*/, double lo, double hi,
+                                              double mid, double inv_half, double y,
+                                              double (&w)[L], unsigned long long* bad) {
+    constexpr LagrangeConsts<L> C;
+    const double slack = 1e-12 * (hi - lo);  // tensor_weights, interpolation.hpp:47-49
+    if (y < lo - slack || y > hi + slack) atomicOr(&bad[1], 1ull);
+    const double t = (y - mid) * inv_half;
+    constexpr double step = 2.0 / (L - 1);
+    double d[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) d[k] = t - (-1.0 + step * k);
+    double pre = C.c[0];
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+        w[k] = pre;
+        if (k + 1 < L) pre = pre * d[k] * (C.c[k + 1 < L ? k + 1 : 0] / C.c[k]);
+    }
+    double suf = 1.0;
+#pragma unroll
+    for (int k = L - 1; k >= 0; --k) {
+        w[k] *= suf;
+        suf *= d[k];
+    }
+}
+
+// First cell c in [cb, ce] with start[c] >= target (start is non-decreasing),
+// found by the whole warp 32 cells at a time.
+__device__ __forceinline__ int warp_lower_bound(const int32_t* start, int cb, int ce, int target,
+                                                int lane) {
+    for (int base = cb; base <= ce; base += 32) {
+        const int c = base + lane;
+        const bool hit = c <= ce && start[c] >= target;
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (m) return base + __ffs(m) - 1;
+    }
+    return ce;
+}
+
+struct CellAxis {
+    double lo, hi, mid, inv;
+};
+__device__ __forceinline__ CellAxis cell_axis(const Geometry& g, int a, int i) {
+    CellAxis c;
+    c.lo = cell_lo(g, a, i);
+    c.hi = cell_hi(g, a, i);
+    c.mid = 0.5 * (c.hi + c.lo);
+    c.inv = 1.0 / (0.5 * (c.hi - c.lo));
+    return c;
+}
+
+// Spread on FP64 tensor cores. For one cell,
+//     phi[i][(j,k)] = sum_p (q_p w0_p[i]) (w1_p[j] w2_p[k])
+// is an (L x L^2) = (L x P)(P x L^2) GEMM over the cell's particles. Each
+// warp owns whole cells; per 16-particle chunk a lane pair (l, l+16) builds
+// one particle's A row (q w0, 8 padded) and B row (w1 (x) w2, NT*8 padded)
+// particle-contiguous in shared memory, then 4 k-steps of m8n8k4 DMMA
+// accumulate phi in registers. The finished grid is contracted with the
+// cell's W2 slice, T1c[(i,j)][r] = sum_k phi[(i,j)][k] W2[r][c2 L + k], on
+// DMMA as well, into the warp's column partial of T1.
+template <int L>
+struct SpreadTile {
+    static constexpr int L2 = L * L;
+    static constexpr int NT = (L2 + 7) / 8;   // n-tiles over (j,k)
+    static constexpr int MT2 = (L2 + 7) / 8;  // m-tiles of the contraction (rows (i,j))
+    static constexpr int KS2 = (L + 3) / 4;   // k-steps of the contraction
+    static constexpr int LDK = KS2 * 4;       // phi[(i,j)][k] row stride
+    static constexpr int CH = 16;             // particles staged per chunk
+    static constexpr int LDP = CH + 4;        // staged row stride (conflict-free fragments)
+    static constexpr int NW = 4;              // warps per CTA
+    static constexpr int stage = (8 + NT * 8) * LDP;
+    static_assert(MT2 * 8 * LDK <= stage, "phi must fit in the staging area");
+};
+
+template <int L>
+__host__ __device__ constexpr int spread_warp_doubles(int R) {
+    return SpreadTile<L>::stage + SpreadTile<L>::MT2 * 8 * ((R + 7) / 8) * 8;
+}
+
+#ifndef SPREAD_MINB
+#define SPREAD_MINB 3
+#endif
+// Staging rows that are identically zero (A rows >= L, B rows >= L^2); the
+// chunk loop never writes them, so they are cleared once per cell reuse.
+template <int L>
+__device__ __forceinline__ void zero_padding(double* As, double* Bs, int lane) {
+    using T = SpreadTile<L>;
+    for (int e = lane; e < (8 - L) * T::LDP; e += 32) As[L * T::LDP + e] = 0.0;
+    for (int e = lane; e < (T::NT * 8 - T::L2) * T::LDP; e += 32) Bs[T::L2 * T::LDP + e] = 0.0;
+}
+
+template <int L>
+__global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, int want_fwd) {
+    using T = SpreadTile<L>;
+    constexpr int L2 = T::L2, L3 = L2 * L, NT = T::NT, LDP = T::LDP, NW = T::NW, CH = T::CH;
+    constexpr int MT2 = T::MT2, KS2 = T::KS2, LDK = T::LDK;
+    const Geometry& g = a.g;
+    const int R = g.R, RT = (R + 7) / 8, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int RP = RT * 8;
+    const ColumnRange cr = column_range(g, a.S);
+    extern __shared__ double sm[];
+    const int per_warp = spread_warp_doubles<L>(R);
+    double* As = sm + warp * per_warp;  // [8][LDP]       q w0, particle-contiguous
+    double* Bs = As + 8 * LDP;          // [NT*8][LDP]    w1 (x) w2
+    double* ph = As;                    // [MT2*8][LDK]   finished cell grid (aliases staging)
+    double* t1w = As + T::stage;        // [MT2*8][RP]    warp partial of T1
+    __shared__ double lc[16];
+    __shared__ double red[128];
+    lagrange_consts(L, lc);
+    for (int e = lane; e < MT2 * 8 * RP; e += 32) t1w[e] = 0.0;
+    const CellAxis ax0 = cell_axis(g, 0, cr.c0), ax1 = cell_axis(g, 1, cr.c1);
+    const int p = lane & (CH - 1), half = lane >> 4;
+    double qsum = 0.0;
+    zero_padding<L>(As, Bs, lane);
+    __syncthreads();
+
+    // Each warp takes a contiguous run of cells holding ~1/NW of the column
+    // segment's particles (a deterministic, data-dependent split).
+    const int col_cell0 = (cr.c0 * g.K[1] + cr.c1) * g.K[2];
+    int zw0, zw1;
+    {
+        const int P0 = a.start[col_cell0 + cr.zb], P1 = a.start[col_cell0 + cr.ze];
+        const int t0 = P0 + (int)((long long)(P1 - P0) * warp / NW);
+        const int t1 = P0 + (int)((long long)(P1 - P0) * (warp + 1) / NW);
+        zw0 = warp == 0 ? cr.zb
+                        : warp_lower_bound(a.start, col_cell0 + cr.zb, col_cell0 + cr.ze, t0, lane) - col_cell0;
+        zw1 = warp == NW - 1 ? cr.ze
+                             : warp_lower_bound(a.start, col_cell0 + cr.zb, col_cell0 + cr.ze, t1, lane) - col_cell0;
+    }
+    int s_next = a.start[col_cell0 + zw0];
+    for (int c2 = zw0; c2 < zw1; ++c2) {
+        const int cell = col_cell0 + c2;
+        const int s0 = s_next, s1 = a.start[cell + 1];
+        s_next = s1;
+        if (s0 == s1) {
+            if (a.phi_cells)
+                for (int node = lane; node < L3; node += 32) a.phi_cells[(int64_t)cell * L3 + node] = 0.0;
+            continue;
+        }
+        const CellAxis ax2 = cell_axis(g, 2, c2);
+        double acc[NT][2];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+        // lanes past the chunk end clamp to a valid particle and carry q = 0
+        double4 nxt = a.sp[s0 + min(p, s1 - s0 - 1)];
+        for (int base = s0; base < s1; base += CH) {
+            const int cnt = min(CH, s1 - base);
+            const double4 pt = nxt;  // software prefetch of the next chunk
+            if (base + CH < s1) nxt = a.sp[base + CH + min(p, s1 - base - CH - 1)];
+            double w0[L], w1[L], w2[L];
+            const double qv = p < cnt ? pt.w : 0.0;
+            qsum += half == 0 ? qv : 0.0;
+            lagrange_fast<L>(lc, ax0.lo, ax0.hi, ax0.mid, ax0.inv, pt.x, w0, a.bad);
+            lagrange_fast<L>(lc, ax1.lo, ax1.hi, ax1.mid, ax1.inv, pt.y, w1, a.bad);
+            lagrange_fast<L>(lc, ax2.lo, ax2.hi, ax2.mid, ax2.inv, pt.z, w2, a.bad);
+            __syncwarp();
+            // lane pair (p, p+16): A rows [4h, 4h+4) and B rows j in [JH h, JH h + JH)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (i < L) {
+                    const double lo_w = w0[i], hi_w = (4 + i < L) ? w0[4 + i < L ? 4 + i : 0] : 0.0;
+                    As[(half * 4 + i) * LDP + p] = qv * (half ? hi_w : lo_w);  // rows >= L get 0
+                }
+            constexpr int JH = (L + 1) / 2;
+#pragma unroll
+            for (int jj = 0; jj < JH; ++jj) {
+                const double a_lo = w1[jj];
+                const double a_hi = (JH + jj < L) ? w1[JH + jj < L ? JH + jj : 0] : 0.0;
+                const double wj = half ? a_hi : a_lo;
+                const int row = (half * JH + jj) * L;
+#pragma unroll
+                for (int kk = 0; kk < L; ++kk) Bs[(row + kk) * LDP + p] = wj * w2[kk];  // rows >= L^2 get 0
+            }
+            __syncwarp();
+            const int ks = (cnt + 3) >> 2;
+            for (int kk = 0; kk < ks; ++kk) {
+                const int col = kk * 4 + (lane & 3);
+                const double af = As[(lane >> 2) * LDP + col];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) dmma884(acc[t], af, Bs[(t * 8 + (lane >> 2)) * LDP + col]);
+            }
+        }
+        __syncwarp();  // staging reads done: reuse it as ph[(i,j)][k]
+        for (int e = lane; e < MT2 * 8 * LDK; e += 32) ph[e] = 0.0;
+        __syncwarp();
+        const int i_row = lane >> 2;
+        if (i_row < L) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int col = t * 8 + 2 * (lane & 3) + c;
+                    if (col < L2) ph[(i_row * L + col / L) * LDK + col % L] = acc[t][c];
+                }
+        }
+        __syncwarp();
+        if (a.phi_cells)
+            for (int node = lane; node < L3; node += 32)
+                a.phi_cells[(int64_t)cell * L3 + node] = ph[(node / L) * LDK + node % L];
+        if (want_fwd) {
+            // T1c = ph[(i,j)][k] (MT2*8 x LDK) . W2s[k][r] (LDK x RP)
+            double bf[KS2][4];
+            const double* w2g = a.W2 + c2 * L;
+#pragma unroll
+            for (int s = 0; s < KS2; ++s)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int k = s * 4 + (lane & 3), r = t * 8 + (lane >> 2);
+                    bf[s][t] = (t < RT && k < L && r < R) ? __ldg(w2g + (int64_t)r * g.n[2] + k) : 0.0;
+                }
+#pragma unroll
+            for (int mt = 0; mt < MT2; ++mt) {
+                double c[4][2];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) c[t][0] = c[t][1] = 0.0;
+#pragma unroll
+                for (int s = 0; s < KS2; ++s) {
+                    const double af = ph[(mt * 8 + (lane >> 2)) * LDK + s * 4 + (lane & 3)];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (t < RT) dmma884(c[t], af, bf[s][t]);
+                }
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (t < RT) {
+                        double* dst = t1w + (mt * 8 + (lane >> 2)) * RP + t * 8 + 2 * (lane & 3);
+                        dst[0] += c[t][0];
+                        dst[1] += c[t][1];
+                    }
+            }
+        }
+        __syncwarp();
+        zero_padding<L>(As, Bs, lane);
+        __syncwarp();
+    }
+    __syncthreads();
+    if (want_fwd) {
+        double* dst = a.T1 + (int64_t)cr.seg * g.n[0] * g.n[1] * R;
+        for (int e = threadIdx.x; e < L2 * R; e += 128) {
+            const int ij = e / R, r = e % R, i = ij / L, j = ij % L;
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) s += sm[w * per_warp + T::stage + ij * RP + r];
+            dst[((int64_t)(cr.c0 * L + i) * g.n[1] + cr.c1 * L + j) * R + r] = s;
+        }
+    }
+    if (a.colq) {
+        red[threadIdx.x] = qsum;
+        __syncthreads();
+        for (int o = 64; o > 0; o >>= 1) {
+            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) a.colq[(int64_t)cr.seg * g.K[0] * g.K[1] + cr.col] = red[0];
+    }
+}
+
+// Backward z-expansion + gather with compile-time L: psi for a batch of the
+// column's cells in shared memory, then one thread per particle,
+// z = sum_i w0[i] sum_j w1[j] sum_k w2[k] psi[i][j][k] - c_Lambda sum(q),
+// scattered straight to global particle order.
+template <int L, int MODE>
+__global__ void __launch_bounds__(256, 3) k_bwd_gather_t(ColumnArgs a, int cells_per_batch) {
+    constexpr int L2 = L * L, L3 = L2 * L;
+    const Geometry& g = a.g;
+    const int R = g.R, tid = threadIdx.x;
+    const ColumnRange cr = column_range(g, a.S);
+    extern __shared__ double sm[];
+    double* b2s = sm;             // L^2 x R
+    double* psi = b2s + L2 * R;   // cells_per_batch x L^3
+    __shared__ double lc[16];
+    lagrange_consts(L, lc);
+    if (MODE != GATHER_FROM_CELLS)
+        for (int e = tid; e < L2 * R; e += 256) {
+            const int ij = e / R, r = e % R, i = ij / L, j = ij % L;
+            b2s[e] = a.B2[((int64_t)(cr.c0 * L + i) * g.n[1] + cr.c1 * L + j) * R + r];
+        }
+    const CellAxis ax0 = cell_axis(g, 0, cr.c0), ax1 = cell_axis(g, 1, cr.c1);
+    const double corr = a.corr ? *a.corr : 0.0;
+    __syncthreads();
+    for (int cb0 = cr.zb; cb0 < cr.ze; cb0 += cells_per_batch) {
+        const int cb1 = min(cr.ze, cb0 + cells_per_batch);
+        const int cell0 = (cr.c0 * g.K[1] + cr.c1) * g.K[2] + cb0;
+        for (int e = tid; e < (cb1 - cb0) * L3; e += 256) {
+            const int b = e / L3, node = e % L3, c2 = cb0 + b;
+            if (MODE == GATHER_FROM_CELLS) {
+                psi[e] = a.psi_cells[(int64_t)(cell0 + b) * L3 + node];
+            } else {
+                const int ij = node / L, k = node % L;
+                const double* wr = a.W2 + c2 * L + k;
+                double s = 0.0;
+                for (int r = 0; r < R; ++r) s = fma(__ldg(wr + (int64_t)r * g.n[2]), b2s[ij * R + r], s);
+                psi[e] = s;
+                if (a.psi_cells) a.psi_cells[(int64_t)(cell0 + b) * L3 + node] = s;
+            }
+        }
+        __syncthreads();
+        if (MODE != PSI_ONLY) {
+            const int s0 = a.start[cell0], s1 = a.start[cell0 + (cb1 - cb0)];
+            double4 pn = s0 + tid < s1 ? a.sp[s0 + tid] : make_double4(0.0, 0.0, 0.0, 0.0);
+            int dn = s0 + tid < s1 ? a.perm[s0 + tid] : 0;
+            for (int s = s0 + tid; s < s1; s += 256) {
+                const double4 p = pn;  // software prefetch of the next particle
+                const int dst = dn;
+                if (s + 256 < s1) {
+                    pn = a.sp[s + 256];
+                    dn = a.perm[s + 256];
+                }
+                const int c2 = axis_cell(p.z, g.center[2], g.radius, g.K[2]);
+                const double* ps = psi + (c2 - cb0) * L3;
+                double w0[L], w1[L], w2[L];
+                const CellAxis ax2 = cell_axis(g, 2, c2);
+                lagrange_fast<L>(lc, ax0.lo, ax0.hi, ax0.mid, ax0.inv, p.x, w0, a.bad);
+                lagrange_fast<L>(lc, ax1.lo, ax1.hi, ax1.mid, ax1.inv, p.y, w1, a.bad);
+                lagrange_fast<L>(lc, ax2.lo, ax2.hi, ax2.mid, ax2.inv, p.z, w2, a.bad);
+                double z = 0.0;
+#pragma unroll
+                for (int i = 0; i < L; ++i) {
+                    double zi = 0.0;
+#pragma unroll
+                    for (int j = 0; j < L; ++j) {
+                        const double* row = ps + (i * L + j) * L;
+                        double zij = 0.0;
+#pragma unroll
+                        for (int k = 0; k < L; ++k) zij = fma(w2[k], row[k], zij);
+                        zi = fma(w1[j], zij, zi);
+                    }
+                    z = fma(w0[i], zi, z);
+                }
+                a.out[dst] = z - corr;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 size_t spread_smem(const Geometry& g) {
     const int L = g.L;
     return sizeof(double) * ((size_t)L * L * L + (size_t)L * L * g.R + (size_t)g.R * L +
@@ -267,8 +663,52 @@ size_t spread_smem(const Geometry& g) {
 
 int gather_batch(const Geometry& g) {
     const int L3 = g.L * g.L * g.L;
-    const int cap = (96 * 1024) / (int)(sizeof(double) * L3);
+    const int cap = (32 * 1024) / (int)(sizeof(double) * L3);
     return cap < 1 ? 1 : cap;
+}
+
+
+template <int L>
+void launch_spread_mma(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
+    const size_t smem = sizeof(double) * SpreadTile<L>::NW * spread_warp_doubles<L>(a.g.R);
+    static int attr_done = 0;
+    if (!attr_done) {
+        KB_CUDA(cudaFuncSetAttribute(k_spread_mma<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+        attr_done = 1;
+    }
+    if (smem > 200 * 1024) throw Error(KPME_GPU_INVALID_ARGUMENT, "spread: tile too large");
+    const int grid = a.g.K[0] * a.g.K[1] * a.S;
+    k_spread_mma<L><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+    KB_CHECK_LAUNCH();
+}
+
+template <int L>
+void launch_gather_t(const ColumnArgs& a, int mode, cudaStream_t s) {
+    static int attr_done = 0;
+    if (!attr_done) {
+        KB_CUDA(cudaFuncSetAttribute(k_bwd_gather_t<L, GATHER_FROM_B2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        KB_CUDA(cudaFuncSetAttribute(k_bwd_gather_t<L, GATHER_FROM_CELLS>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        KB_CUDA(cudaFuncSetAttribute(k_bwd_gather_t<L, PSI_ONLY>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_done = 1;
+    }
+    const int grid = a.g.K[0] * a.g.K[1] * a.S;
+    const int cb = gather_batch(a.g);
+    const size_t smem = sizeof(double) * ((size_t)L * L * a.g.R + (size_t)cb * L * L * L);
+    switch (mode) {
+        case GATHER_FROM_B2:
+            k_bwd_gather_t<L, GATHER_FROM_B2><<<grid, 256, smem, s>>>(a, cb);
+            break;
+        case GATHER_FROM_CELLS:
+            k_bwd_gather_t<L, GATHER_FROM_CELLS><<<grid, 256, smem, s>>>(a, cb);
+            break;
+        default:
+            k_bwd_gather_t<L, PSI_ONLY><<<grid, 256, smem, s>>>(a, cb);
+    }
+    KB_CHECK_LAUNCH();
 }
 
 }  // namespace
@@ -281,6 +721,17 @@ void launch_spread_fwd(const ColumnArgs& a, int mode, bool want_fwd, cudaStream_
         KB_CUDA(cudaFuncSetAttribute(k_spread_fwd<SPREAD_FROM_CELLS>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
+    }
+    if (mode == SPREAD_PARTICLES && a.g.L <= 8) {
+        switch (a.g.L) {
+            case 2: return launch_spread_mma<2>(a, want_fwd, s);
+            case 3: return launch_spread_mma<3>(a, want_fwd, s);
+            case 4: return launch_spread_mma<4>(a, want_fwd, s);
+            case 5: return launch_spread_mma<5>(a, want_fwd, s);
+            case 6: return launch_spread_mma<6>(a, want_fwd, s);
+            case 7: return launch_spread_mma<7>(a, want_fwd, s);
+            default: return launch_spread_mma<8>(a, want_fwd, s);
+        }
     }
     const int grid = a.g.K[0] * a.g.K[1] * a.S;
     const size_t smem = spread_smem(a.g);
@@ -301,6 +752,18 @@ void launch_bwd_gather(const ColumnArgs& a, int mode, cudaStream_t s) {
         KB_CUDA(cudaFuncSetAttribute(k_bwd_gather<PSI_ONLY>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
+    }
+    switch (a.g.L) {
+        case 2: return launch_gather_t<2>(a, mode, s);
+        case 3: return launch_gather_t<3>(a, mode, s);
+        case 4: return launch_gather_t<4>(a, mode, s);
+        case 5: return launch_gather_t<5>(a, mode, s);
+        case 6: return launch_gather_t<6>(a, mode, s);
+        case 7: return launch_gather_t<7>(a, mode, s);
+        case 8: return launch_gather_t<8>(a, mode, s);
+        case 10: return launch_gather_t<10>(a, mode, s);
+        case 12: return launch_gather_t<12>(a, mode, s);
+        default: break;
     }
     const int grid = a.g.K[0] * a.g.K[1] * a.S;
     const int cb = gather_batch(a.g);

@@ -260,7 +260,7 @@ extern "C" int kpme_gpu_plan_create(const kpme_gpu_config* cfg, int64_t max_part
             p->form = cfg->formulation == KPME_GPU_FORM_DENSE ? KPME_GPU_FORM_DENSE
                                                               : KPME_GPU_FORM_COLLAPSED;
             const int ncol = g.K[0] * g.K[1];
-            p->S = std::max(1, std::min(g.z_hi - g.z_lo, (2 * 148 + ncol - 1) / ncol));
+            p->S = std::max(1, std::min(g.z_hi - g.z_lo, (4 * 148 + ncol - 1) / ncol));
 
             const int P = 2 * g.M + 1;
             p->tw = p->alloc<double>(std::max(1, p->nterms));
@@ -283,6 +283,7 @@ extern "C" int kpme_gpu_plan_create(const kpme_gpu_config* cfg, int64_t max_part
             p->sb.cnt = p->alloc<int32_t>(g.ncell);
             p->sb.start = p->alloc<int32_t>(g.ncell + 1);
             p->sb.key = p->alloc<int32_t>(p->cap);
+            p->sb.rank = p->alloc<int32_t>(p->cap);
             p->sb.perm = p->alloc<int32_t>(p->cap);
             p->sb.big = p->alloc<int32_t>(g.ncell);
             p->sb.nbig = p->alloc<int32_t>(1);
@@ -325,11 +326,8 @@ extern "C" int kpme_gpu_plan_set_stream(kpme_gpu_plan p, void* stream) {
             p->gexec = nullptr;
         }
         if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
-        p->own_stream = stream == nullptr;
-        if (stream)
-            p->stream = static_cast<cudaStream_t>(stream);
-        else
-            KB_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+        p->own_stream = false;
+        p->stream = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
     });
 }
 

@@ -1,8 +1,8 @@
 // sort.cu -- bit-exact cell sort (assign_particles, geometry.hpp:131-154).
 //
-// Pipeline: cell key + box check + histogram (integer atomics only) ->
-// exclusive scan -> scatter into cell segments -> per-cell sort of the
-// member indices. The last step restores the reference's "ascending particle
+// Pipeline: cell key + box check + histogram whose atomic also hands each
+// particle a provisional slot in its cell (integer atomics only) -> exclusive
+// scan -> placement into cell segments -> per-cell sort of the member indices. The last step restores the reference's "ascending particle
 // index within each cell" order (Partition.members, geometry.hpp:124-127), so
 // the result is identical to the reference whatever order the atomics ran in.
 #include <climits>
@@ -29,8 +29,8 @@ __device__ __forceinline__ int axis_cell(double p, double c, double r, int K) {
 }
 
 __global__ void k_keys(Geometry g, int64_t n, const double* __restrict__ xyz,
-                       int32_t* __restrict__ key, int32_t* __restrict__ cnt,
-                       unsigned long long* bad) {
+                       int32_t* __restrict__ key, int32_t* __restrict__ rank,
+                       int32_t* __restrict__ cnt, unsigned long long* bad) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const double p0 = xyz[3 * i], p1 = xyz[3 * i + 1], p2 = xyz[3 * i + 2];
@@ -44,50 +44,90 @@ __global__ void k_keys(Geometry g, int64_t n, const double* __restrict__ xyz,
         if (c2 < g.z_lo || c2 >= g.z_hi) atomicOr(&bad[1], 2ull);  // not in this slab
         const int k = (c0 * g.K[1] + c1) * g.K[2] + c2;  // CellGrid::flatten
         key[i] = k;
-        atomicAdd(&cnt[k], 1);
+        rank[i] = atomicAdd(&cnt[k], 1);  // provisional slot, fixed up by k_segsort
     }
 }
 
-// Exclusive scan of the histogram by one CTA; leaves start[] and resets cnt[]
-// to the running cursor.
-__global__ void k_scan(int ncell, int32_t* __restrict__ cnt, int32_t* __restrict__ start) {
+// Exclusive scan of the histogram by one CTA, in shared-memory chunks of
+// kScanChunk counts (coalesced loads, all in flight); leaves start[] and
+// resets cnt[] to the running cursor.
+constexpr int kScanChunk = 16384;
+__global__ void __launch_bounds__(1024) k_scan(int ncell, int32_t* __restrict__ cnt,
+                                               int32_t* __restrict__ start) {
+    extern __shared__ int32_t sc[];  // kScanChunk
     __shared__ int32_t wsum[32];
+    __shared__ int32_t carry;
     const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int per = (ncell + T - 1) / T;
-    const int b = min(tid * per, ncell), e = min(b + per, ncell);
-    int local = 0;
-    for (int i = b; i < e; ++i) local += cnt[i];
-    int x = local;
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[w] = x;
-    __syncthreads();
-    if (w == 0) {
-        int v = lane < (T >> 5) ? wsum[lane] : 0;
+    constexpr int per = kScanChunk / 1024;
+    if (tid == 0) carry = 0;
+    for (int base = 0; base < ncell; base += kScanChunk) {
+        const int m = min(kScanChunk, ncell - base);
+        for (int i = tid; i < kScanChunk; i += T) sc[i] = i < m ? cnt[base + i] : 0;
+        __syncthreads();
+        int local = 0;
+#pragma unroll
+        for (int k = 0; k < per; ++k) local += sc[tid * per + k];
+        int x = local;
         for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += y;
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
-        wsum[lane] = v;
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int v = lane < (T >> 5) ? wsum[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += y;
+            }
+            wsum[lane] = v;
+        }
+        __syncthreads();
+        int run = carry + x - local + (w > 0 ? wsum[w - 1] : 0);
+#pragma unroll
+        for (int k = 0; k < per; ++k) {
+            const int c = sc[tid * per + k];
+            sc[tid * per + k] = run;
+            run += c;
+        }
+        __syncthreads();
+        for (int i = tid; i < m; i += T) {
+            start[base + i] = sc[i];
+            cnt[base + i] = sc[i];
+        }
+        if (tid == T - 1) carry = run;
+        __syncthreads();
     }
-    __syncthreads();
-    int run = x - local + (w > 0 ? wsum[w - 1] : 0);
-    for (int i = b; i < e; ++i) {
-        const int c = cnt[i];
-        start[i] = run;
-        cnt[i] = run;
-        run += c;
-    }
-    if (tid == T - 1) start[ncell] = run;
+    if (tid == 0) start[ncell] = carry;
 }
 
-__global__ void k_scatter(int64_t n, const int32_t* __restrict__ key, int32_t* cursor,
-                          int32_t* __restrict__ perm) {
+__global__ void k_place(int64_t n, const int32_t* __restrict__ key,
+                        const int32_t* __restrict__ rank, const int32_t* __restrict__ start,
+                        int32_t* __restrict__ perm) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        perm[atomicAdd(&cursor[key[i]], 1)] = (int32_t)i;
+        perm[start[key[i]] + rank[i]] = (int32_t)i;
+}
+
+// Warp rank sort of b[0..cnt) (distinct values, padded to P4 with INT_MAX):
+// member k of lane l goes to out[number of smaller members].
+template <int V>
+__device__ __forceinline__ void rank_sort(const int32_t* b, int P4, int cnt, int lane,
+                                          int32_t* out) {
+    int v[V], r[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        v[k] = (lane + 32 * k < cnt) ? b[lane + 32 * k] : INT_MAX;
+        r[k] = 0;
+    }
+    for (int j = 0; j < P4; j += 4) {
+        const int4 x = *reinterpret_cast<const int4*>(b + j);
+#pragma unroll
+        for (int k = 0; k < V; ++k) r[k] += (x.x < v[k]) + (x.y < v[k]) + (x.z < v[k]) + (x.w < v[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+        if (lane + 32 * k < cnt) out[r[k]] = v[k];
 }
 
 // One warp per cell: restore ascending member order.
@@ -95,7 +135,7 @@ __global__ void __launch_bounds__(256) k_segsort_warp(int ncell, const int32_t* 
                                                       int32_t* __restrict__ perm,
                                                       int32_t* __restrict__ big,
                                                       int32_t* __restrict__ nbig) {
-    __shared__ int32_t buf[8][kWarpCap];
+    __shared__ __align__(16) int32_t buf[8][kWarpCap];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cell = blockIdx.x * 8 + w;
     if (cell >= ncell) return;
@@ -116,9 +156,18 @@ __global__ void __launch_bounds__(256) k_segsort_warp(int ncell, const int32_t* 
         if (lane < cnt) perm[s0 + lane] = v;
         return;
     }
-    int P = 64;
-    while (P < cnt) P <<= 1;
     int32_t* b = buf[w];
+    if (cnt <= 256) {
+        // rank by counting: each member's slot = number of smaller members
+        const int P4 = (cnt + 3) & ~3;
+        for (int i = lane; i < P4; i += 32) b[i] = i < cnt ? perm[s0 + i] : INT_MAX;
+        __syncwarp();
+        if (cnt <= 128) rank_sort<4>(b, P4, cnt, lane, perm + s0);
+        else rank_sort<8>(b, P4, cnt, lane, perm + s0);
+        return;
+    }
+    int P = 512;
+    while (P < cnt) P <<= 1;
     for (int i = lane; i < P; i += 32) b[i] = i < cnt ? perm[s0 + i] : INT_MAX;
     __syncwarp();
     for (int k = 2; k <= P; k <<= 1)
@@ -223,19 +272,21 @@ void launch_sort(const Geometry& g, int64_t n, const double* xyz, const SortBuff
     if (!attr_set) {
         KB_CUDA(cudaFuncSetAttribute(k_segsort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kBlockCap * (int)sizeof(int32_t)));
+        KB_CUDA(cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kScanChunk * (int)sizeof(int32_t)));
         attr_set = true;
     }
     KB_CUDA(cudaMemsetAsync(b.cnt, 0, sizeof(int32_t) * g.ncell, s));
     KB_CUDA(cudaMemsetAsync(b.nbig, 0, sizeof(int32_t), s));
     if (n > 0) {
-        k_keys<<<grid_for(n, 256), 256, 0, s>>>(g, n, xyz, b.key, b.cnt, b.bad);
+        k_keys<<<grid_for(n, 256), 256, 0, s>>>(g, n, xyz, b.key, b.rank, b.cnt, b.bad);
         KB_CHECK_LAUNCH();
     }
-    k_scan<<<1, 1024, 0, s>>>(g.ncell, b.cnt, b.start);
+    k_scan<<<1, 1024, kScanChunk * sizeof(int32_t), s>>>(g.ncell, b.cnt, b.start);
     KB_CHECK_LAUNCH();
     int l = 2;
     if (n > 0) {
-        k_scatter<<<grid_for(n, 256), 256, 0, s>>>(n, b.key, b.cnt, b.perm);
+        k_place<<<grid_for(n, 256), 256, 0, s>>>(n, b.key, b.rank, b.start, b.perm);
         KB_CHECK_LAUNCH();
         k_segsort_warp<<<(g.ncell + 7) / 8, 256, 0, s>>>(g.ncell, b.start, b.perm, b.big, b.nbig);
         KB_CHECK_LAUNCH();

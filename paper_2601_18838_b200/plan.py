@@ -27,7 +27,12 @@ def _ptr(t: torch.Tensor | None):
 
 
 class KpmePlan:
-    """Plan for repeated kpme_apply calls on one cell grid and decomposition."""
+    """Plan for repeated kpme_apply calls on one cell grid and decomposition.
+
+    The plan runs on its own torch stream (``self.stream``); every call first
+    makes that stream wait for the caller's current stream and afterwards
+    makes the caller's stream wait for it, so results order with surrounding
+    torch work while graph capture stays possible."""
 
     def __init__(self, cfg: EwaldConfig, grid: CellGrid, order: int, dec: SkpDecomposition,
                  max_particles: int, opt: KpmeOptions | None = None, device: int = 0,
@@ -42,7 +47,14 @@ class KpmePlan:
         with torch.cuda.device(device):
             check(lib.kpme_gpu_plan_create(C.byref(self._c), self.max_particles,
                                            C.byref(self._h)))
-        self.bind_stream()
+        self.stream = torch.cuda.Stream(device=device)
+        check(lib.kpme_gpu_plan_set_stream(self._h, C.c_void_p(self.stream.cuda_stream)))
+
+    def _enter(self):
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+
+    def _leave(self):
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
 
     def close(self):
         if self._h:
@@ -63,10 +75,6 @@ class KpmePlan:
     def grid_size(self) -> int:
         return self.order ** 3
 
-    def bind_stream(self, stream: torch.cuda.Stream | None = None):
-        s = stream or torch.cuda.current_stream(self.device)
-        check(lib.kpme_gpu_plan_set_stream(self._h, C.c_void_p(s.cuda_stream)))
-
     # ---- full pipeline --------------------------------------------------
     def execute(self, xyz: torch.Tensor, q: torch.Tensor, out: torch.Tensor | None = None,
                 defer_checks: bool = False) -> torch.Tensor:
@@ -74,12 +82,20 @@ class KpmePlan:
         if out is None:
             out = torch.empty(n, dtype=torch.float64, device=xyz.device)
         flags = _lib.DEFER_CHECKS if defer_checks else 0
+        self._enter()
         check(lib.kpme_gpu_plan_execute_device(self._h, n, _ptr(xyz), _ptr(q), _ptr(out), flags))
+        self._leave()
         return out
 
-    def execute_graph(self, xyz: torch.Tensor, q: torch.Tensor, out: torch.Tensor):
+    def execute_graph(self, xyz: torch.Tensor, q: torch.Tensor, out: torch.Tensor,
+                      sync_caller: bool = True):
+        """Replay the captured pipeline (captured on first use / new pointers)."""
+        if sync_caller:
+            self._enter()
         check(lib.kpme_gpu_plan_graph_execute(self._h, xyz.shape[0], _ptr(xyz), _ptr(q),
                                               _ptr(out)))
+        if sync_caller:
+            self._leave()
         return out
 
     def execute_host(self, xyz: np.ndarray, q: np.ndarray, out: np.ndarray | None = None):
@@ -90,6 +106,7 @@ class KpmePlan:
         if out is None:
             out = np.zeros(max(n, 1))
         dp = C.POINTER(C.c_double)
+        self._enter()
         check(lib.kpme_gpu_plan_execute(self._h, n, xyz.ctypes.data_as(dp), q.ctypes.data_as(dp),
                                         out.ctypes.data_as(dp)))
         return out[:n]
@@ -97,6 +114,7 @@ class KpmePlan:
     def execute_host_ptr(self, n: int, xyz_ptr: int, q_ptr: int, out_ptr: int):
         """Host-pointer variant for pinned torch CPU tensors."""
         dp = C.POINTER(C.c_double)
+        self._enter()
         check(lib.kpme_gpu_plan_execute(self._h, n, C.cast(xyz_ptr, dp), C.cast(q_ptr, dp),
                                         C.cast(out_ptr, dp)))
 
@@ -121,26 +139,34 @@ class KpmePlan:
         n = xyz.shape[0]
         perm = torch.empty(max(n, 1), dtype=torch.int32, device=xyz.device)
         start = torch.empty(self.ncell + 1, dtype=torch.int32, device=xyz.device)
+        self._enter()
         check(lib.kpme_gpu_sort(self._h, n, _ptr(xyz), _ptr(perm), _ptr(start)))
+        self._leave()
         return perm[:n], start
 
     def spread(self, xyz: torch.Tensor, q: torch.Tensor) -> torch.Tensor:
         """InterpOperator::interpolate (interpolation.hpp:84-92): [ncell, L^3]."""
         phi = torch.empty(self.ncell, self.grid_size, dtype=torch.float64, device=xyz.device)
+        self._enter()
         check(lib.kpme_gpu_spread(self._h, xyz.shape[0], _ptr(xyz), _ptr(q), _ptr(phi)))
+        self._leave()
         return phi
 
     def skp_apply(self, phi: torch.Tensor) -> torch.Tensor:
         """spkmv_sum over all terms (parallel.hpp:184-228)."""
         psi = torch.empty_like(phi)
+        self._enter()
         check(lib.kpme_gpu_skp_apply(self._h, _ptr(phi.contiguous()), _ptr(psi)))
+        self._leave()
         return psi
 
     def gather(self, xyz: torch.Tensor, psi: torch.Tensor) -> torch.Tensor:
         """InterpOperator::anterpolate (interpolation.hpp:95-105)."""
         out = torch.empty(xyz.shape[0], dtype=torch.float64, device=xyz.device)
+        self._enter()
         check(lib.kpme_gpu_gather(self._h, xyz.shape[0], _ptr(xyz), _ptr(psi.contiguous()),
                                   _ptr(out)))
+        self._leave()
         return out
 
     def axis_operands(self, axis: int) -> torch.Tensor:
@@ -148,7 +174,9 @@ class KpmePlan:
         n = self.grid.counts[axis] * self.order
         out = torch.empty(max(len(self.dec.terms), 1), n, n, dtype=torch.float64,
                           device=f"cuda:{self.device}")
+        self._enter()
         check(lib.kpme_gpu_plan_axis_operands(self._h, axis, _ptr(out)))
+        self._leave()
         return out[: len(self.dec.terms)]
 
 

@@ -150,6 +150,24 @@ int kpme_gpu_plan_enable_timing(kpme_gpu_plan plan, int on);
 int kpme_gpu_plan_stage_times(kpme_gpu_plan plan, double* ms, int cap,
                               int* count);
 
+/* ---- z-slab plans (multi-GPU, one process per GPU) ---------------------- */
+/* A plan owning cell planes [z_lo, z_hi) along axis 2 (the slab of one
+ * rank). Particles passed to it must lie in the slab (else
+ * KPME_GPU_INVALID_ARGUMENT at the next status check). The collapsed form's
+ * only exchange is a sum over ranks of the R^3 + 1 core (R = 2M+1; the last
+ * entry carries sum(q)), done by the caller between the two halves below --
+ * the distributed counterpart of the axis-group reductions of spkmv
+ * (parallel.hpp:169-176) and allreduce_scalar (parallel.hpp:254-257). */
+int kpme_gpu_plan_create_slab(const kpme_gpu_config* cfg, int64_t max_particles,
+                              int z_lo, int z_hi, kpme_gpu_plan* out);
+int kpme_gpu_plan_core_size(kpme_gpu_plan plan);
+/* sort .. forward contractions: d_core[R^3 + 1] = this slab's partial core */
+int kpme_gpu_plan_forward(kpme_gpu_plan plan, int64_t n, const double* d_xyz,
+                          const double* d_q, double* d_core);
+/* core (summed over slabs) -> backward contractions -> gather - c*sum(q) */
+int kpme_gpu_plan_backward(kpme_gpu_plan plan, const double* d_core,
+                           double* d_potentials);
+
 /* ---- stage entry points (device buffers, plan stream) ------------------ */
 /* assign_particles (geometry.hpp:131-154), bit-exact: perm[n] is the
  * concatenation of Partition.members in flattened cell order,

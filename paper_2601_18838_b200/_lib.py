@@ -91,6 +91,11 @@ def _load():
                                                  P, P, P, P, P, P, C.c_size_t]),
         "kpme_gpu_plan_axis_operands": (C.c_int, [P, C.c_int, P]),
         "kpme_gpu_dgemm_tn": (C.c_int, [P, C.c_int64, C.c_int64, C.c_int64, P, P, P, C.c_int]),
+        "kpme_gpu_plan_create_slab": (C.c_int, [C.POINTER(Config), C.c_int64, C.c_int, C.c_int,
+                                                C.POINTER(P)]),
+        "kpme_gpu_plan_core_size": (C.c_int, [P]),
+        "kpme_gpu_plan_forward": (C.c_int, [P, C.c_int64, P, P, P]),
+        "kpme_gpu_plan_backward": (C.c_int, [P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -112,7 +117,8 @@ EXPORTS = sorted(
         "kpme_gpu_plan_enable_timing", "kpme_gpu_plan_stage_times", "kpme_gpu_sort",
         "kpme_gpu_spread", "kpme_gpu_skp_apply", "kpme_gpu_gather",
         "kpme_gpu_dense_workspace_bytes", "kpme_gpu_kron_matvec_dense",
-        "kpme_gpu_plan_axis_operands", "kpme_gpu_dgemm_tn",
+        "kpme_gpu_plan_axis_operands", "kpme_gpu_dgemm_tn", "kpme_gpu_plan_create_slab",
+        "kpme_gpu_plan_core_size", "kpme_gpu_plan_forward", "kpme_gpu_plan_backward",
     ]
 )
 

@@ -34,6 +34,7 @@ struct kpme_gpu_plan_s {
     int S = 1;
     int form = KPME_GPU_FORM_COLLAPSED;
     int launches = 0;
+    int64_t last_n = 0;
 
     // factor tables
     double* tw = nullptr;
@@ -210,6 +211,30 @@ void pipeline(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q, do
     p->launches += 5;
 }
 
+// First half for slab plans: sort .. forward contractions into core.
+void forward_half(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q, double* core) {
+    if (n > p->cap) invalid("kpme_gpu: more particles than the plan was created for");
+    if (p->form == KPME_GPU_FORM_DENSE)
+        invalid("kpme_gpu: slab plans use the collapsed formulation");
+    p->launches = 0;
+    reset_flags(p);
+    sort_and_permute(p, n, xyz, q);
+    kb::ColumnArgs a = column_args(p);
+    kb::launch_spread_fwd(a, kb::SPREAD_PARTICLES, true, p->stream);
+    kb::launch_core_forward(p->g, p->S, p->T1, p->W[0], p->W[1], p->T2, p->colq, core, p->stream);
+    p->last_n = n;
+    p->launches += 3;
+}
+
+void backward_half(kpme_gpu_plan p, const double* core, double* out) {
+    kb::launch_core_backward(p->g, p->G, core, p->correction, p->W[0], p->W[1], p->B2, p->corr,
+                             p->stream);
+    kb::ColumnArgs a = column_args(p);
+    a.out = out;
+    kb::launch_bwd_gather(a, kb::GATHER_FROM_B2, p->stream);
+    p->launches += 2;
+}
+
 void collect_times(kpme_gpu_plan p) {
     if (!p->timing) return;
     KB_CUDA(cudaEventSynchronize(p->ev[4]));
@@ -223,9 +248,54 @@ void collect_times(kpme_gpu_plan p) {
 
 }  // namespace
 
+namespace {
+void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, int z_hi,
+                 kpme_gpu_plan* out);
+}
+
 extern "C" int kpme_gpu_plan_create(const kpme_gpu_config* cfg, int64_t max_particles,
                                     kpme_gpu_plan* out) {
     return guarded([&] {
+        validate(cfg);
+        create_plan(cfg, max_particles, 0, cfg->counts[2], out);
+    });
+}
+
+extern "C" int kpme_gpu_plan_create_slab(const kpme_gpu_config* cfg, int64_t max_particles,
+                                         int z_lo, int z_hi, kpme_gpu_plan* out) {
+    return guarded([&] {
+        validate(cfg);
+        if (z_lo < 0 || z_hi < z_lo || z_hi > cfg->counts[2])
+            invalid("kpme_gpu_plan_create_slab: slab outside the cell grid");
+        create_plan(cfg, max_particles, z_lo, z_hi, out);
+    });
+}
+
+extern "C" int kpme_gpu_plan_core_size(kpme_gpu_plan p) {
+    return p ? p->g.R * p->g.R * p->g.R + 1 : -1;
+}
+
+extern "C" int kpme_gpu_plan_forward(kpme_gpu_plan p, int64_t n, const double* xyz,
+                                     const double* q, double* core) {
+    return guarded([&] {
+        if (!p) invalid("kpme_gpu: null plan");
+        KB_CUDA(cudaSetDevice(p->device));
+        forward_half(p, n, xyz, q, core);
+    });
+}
+
+extern "C" int kpme_gpu_plan_backward(kpme_gpu_plan p, const double* core, double* out) {
+    return guarded([&] {
+        if (!p) invalid("kpme_gpu: null plan");
+        KB_CUDA(cudaSetDevice(p->device));
+        backward_half(p, core, out);
+    });
+}
+
+namespace {
+void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, int z_hi,
+                 kpme_gpu_plan* out) {
+    {
         validate(cfg);
         if (!out) invalid("kpme_gpu_plan_create: null output");
         if (max_particles < 0) invalid("kpme_gpu_plan_create: negative particle capacity");
@@ -247,8 +317,8 @@ extern "C" int kpme_gpu_plan_create(const kpme_gpu_config* cfg, int64_t max_part
             g.M = cfg->modes;
             g.R = 2 * cfg->modes + 1;
             g.ncell = cfg->counts[0] * cfg->counts[1] * cfg->counts[2];
-            g.z_lo = 0;
-            g.z_hi = cfg->counts[2];
+            g.z_lo = z_lo;
+            g.z_hi = z_hi;
             const int L = g.L, R = g.R;
             const size_t smem_spread =
                 sizeof(double) * ((size_t)L * L * L + (size_t)L * L * R + (size_t)R * L + 64 * 3 * L);
@@ -260,7 +330,7 @@ extern "C" int kpme_gpu_plan_create(const kpme_gpu_config* cfg, int64_t max_part
             p->form = cfg->formulation == KPME_GPU_FORM_DENSE ? KPME_GPU_FORM_DENSE
                                                               : KPME_GPU_FORM_COLLAPSED;
             const int ncol = g.K[0] * g.K[1];
-            p->S = std::max(1, std::min(g.z_hi - g.z_lo, (4 * 148 + ncol - 1) / ncol));
+            p->S = std::max(1, std::min(std::max(1, g.z_hi - g.z_lo), (4 * 148 + ncol - 1) / ncol));
 
             const int P = 2 * g.M + 1;
             p->tw = p->alloc<double>(std::max(1, p->nterms));
@@ -311,8 +381,9 @@ extern "C" int kpme_gpu_plan_create(const kpme_gpu_config* cfg, int64_t max_part
             delete p;
             throw;
         }
-    });
+    }
 }
+}  // namespace
 
 extern "C" int kpme_gpu_plan_destroy(kpme_gpu_plan plan) {
     return guarded([&] { delete plan; });

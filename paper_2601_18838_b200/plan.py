@@ -1,8 +1,8 @@
 """Steady-state plan API over torch device tensors (kpme_gpu_plan_*).
 
-torch supplies device memory and the stream; every kernel is ours
-(libkpme_b200.so). The plan runs on torch's current CUDA stream so it orders
-with surrounding torch work.
+torch supplies device memory and streams; every kernel is ours
+(libkpme_b200.so). Each plan runs on its own stream, ordered against the
+caller's current stream on entry and exit of every call.
 """
 from __future__ import annotations
 
@@ -36,7 +36,7 @@ class KpmePlan:
 
     def __init__(self, cfg: EwaldConfig, grid: CellGrid, order: int, dec: SkpDecomposition,
                  max_particles: int, opt: KpmeOptions | None = None, device: int = 0,
-                 formulation: str = "auto"):
+                 formulation: str = "auto", slab: tuple | None = None):
         if dec.modes != cfg.modes:
             raise ValueError("kpme_apply: decomposition mode bound mismatch")
         self.cfg, self.grid, self.order, self.dec = cfg, grid, order, dec
@@ -44,9 +44,14 @@ class KpmePlan:
         self.max_particles = int(max_particles)
         self._c, self._keep = make_config(cfg, grid, order, dec, opt, device, formulation)
         self._h = C.c_void_p()
+        self.slab = slab
         with torch.cuda.device(device):
-            check(lib.kpme_gpu_plan_create(C.byref(self._c), self.max_particles,
-                                           C.byref(self._h)))
+            if slab is None:
+                check(lib.kpme_gpu_plan_create(C.byref(self._c), self.max_particles,
+                                               C.byref(self._h)))
+            else:
+                check(lib.kpme_gpu_plan_create_slab(C.byref(self._c), self.max_particles,
+                                                    int(slab[0]), int(slab[1]), C.byref(self._h)))
         self.stream = torch.cuda.Stream(device=device)
         check(lib.kpme_gpu_plan_set_stream(self._h, C.c_void_p(self.stream.cuda_stream)))
 
@@ -117,6 +122,24 @@ class KpmePlan:
         self._enter()
         check(lib.kpme_gpu_plan_execute(self._h, n, C.cast(xyz_ptr, dp), C.cast(q_ptr, dp),
                                         C.cast(out_ptr, dp)))
+
+    # ---- slab halves (multi-GPU) ----------------------------------------
+    def core_size(self) -> int:
+        return int(lib.kpme_gpu_plan_core_size(self._h))
+
+    def forward(self, xyz: torch.Tensor, q: torch.Tensor, core: torch.Tensor) -> torch.Tensor:
+        """This slab's partial R^3 + 1 core (last entry: local sum of q)."""
+        self._enter()
+        check(lib.kpme_gpu_plan_forward(self._h, xyz.shape[0], _ptr(xyz), _ptr(q), _ptr(core)))
+        self._leave()
+        return core
+
+    def backward(self, core: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        """Potentials of this slab's particles from the rank-summed core."""
+        self._enter()
+        check(lib.kpme_gpu_plan_backward(self._h, _ptr(core), _ptr(out)))
+        self._leave()
+        return out
 
     def status(self):
         check(lib.kpme_gpu_plan_status(self._h))

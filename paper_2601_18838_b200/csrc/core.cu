@@ -164,6 +164,26 @@ __global__ void k_core_c(Geometry g, const double* __restrict__ G, const double*
     if (x == 0 && threadIdx.x == 0) *corr = correction * F[R * RR];
 }
 
+// F[e] = sum_b Fpart[e][b] (entry-major partials): one warp per entry, lanes
+// over blocks, fixed shuffle tree (deterministic).
+__global__ void k_core_sum(int nblocks, int E, const double* __restrict__ Fpart,
+                           double* __restrict__ F) {
+    const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (e >= E) return;
+    const double* row = Fpart + (int64_t)e * nblocks;
+    double s0 = 0.0, s1 = 0.0;
+    int b = lane;
+    for (; b + 32 < nblocks; b += 64) {
+        s0 += row[b];
+        s1 += row[b + 32];
+    }
+    if (b < nblocks) s0 += row[b];
+    double s = s0 + s1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) F[e] = s;
+}
+
 __global__ void k_charge_correction(Geometry g, int S, const double* __restrict__ colq,
                                     double correction, double* __restrict__ corr) {
     __shared__ double red[128];
@@ -242,6 +262,13 @@ void launch_core_backward(const Geometry& g, const double* G, const double* F, d
                           cudaStream_t s) {
     const size_t sh = sizeof(double) * ((size_t)g.R * g.R * (g.R + 1) + (size_t)g.R * g.n[1] + g.R);
     k_core_c<<<g.n[0], 256, sh, s>>>(g, G, F, correction, W0, W1, B2, corr);
+    KB_CHECK_LAUNCH();
+}
+
+void launch_core_sum(const Geometry& g, int nblocks, const double* Fpart, double* F,
+                     cudaStream_t s) {
+    const int E = g.R * g.R * g.R + 1;
+    k_core_sum<<<(E + 7) / 8, 256, 0, s>>>(nblocks, E, Fpart, F);
     KB_CHECK_LAUNCH();
 }
 

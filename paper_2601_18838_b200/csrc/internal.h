@@ -54,8 +54,9 @@ struct SortBuffers {
     int32_t* nbig;        // [1]
     unsigned long long* bad;  // [2]: lowest out-of-box index, out-of-cell flag
 };
+// Also writes the sorted particles sp (x, y, z, q) when q and sp are given.
 void launch_sort(const Geometry& g, int64_t n, const double* xyz, const SortBuffers& b,
-                 cudaStream_t s, int* launches);
+                 cudaStream_t s, int* launches, const double* q = nullptr, double4* sp = nullptr);
 void launch_permute(int64_t n, const double* xyz, const double* q, const int32_t* perm,
                     double4* sp, cudaStream_t s);
 
@@ -76,6 +77,14 @@ struct ColumnArgs {
     const int32_t* perm;     // sorted slot -> particle index
     double* out;             // potentials in particle order
     unsigned long long* bad;
+    // fused core (hot path): spread writes per-column partial cores, gather
+    // rebuilds its B2 block from the summed core
+    const double* W0;        // [R][n0]
+    const double* W1;        // [R][n1]
+    double* Fpart;           // [S*K0*K1][R^3+1] partial cores (last entry: sum q)
+    const double* Gc;        // [R^3] collapsed SKP core
+    const double* Fc;        // [R^3+1] summed core
+    double correction;       // c_Lambda
 };
 enum SpreadMode { SPREAD_PARTICLES = 0, SPREAD_FROM_CELLS = 1 };
 enum GatherMode { GATHER_FROM_B2 = 0, GATHER_FROM_CELLS = 1, PSI_ONLY = 2 };
@@ -92,6 +101,9 @@ void launch_core_forward(const Geometry& g, int S, const double* T1, const doubl
 void launch_core_backward(const Geometry& g, const double* G, const double* F,
                           double correction, const double* W0, const double* W1, double* B2,
                           double* corr_out, cudaStream_t s);
+// F[e] = sum_b Fpart[b][e] over nblocks partial cores, blocks in order
+void launch_core_sum(const Geometry& g, int nblocks, const double* Fpart, double* F,
+                     cudaStream_t s);
 // corr = correction * sum(colq), columns in order
 void launch_charge_correction(const Geometry& g, int S, const double* colq, double correction,
                               double* corr, cudaStream_t s);

@@ -555,6 +555,51 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
         __syncwarp();
     }
     __syncthreads();
+    red[threadIdx.x] = qsum;
+    if (want_fwd && a.Fpart) {
+        // Fused y, x contractions: this column segment's partial core
+        //   Fcol[r0][r1][r2] = sum_{i,j} W0[r0][x_i] W1[r1][y_j] T1col[(i,j)][r2]
+        // (the V_1, V_0 phases of spkmv restricted to one column; summed over
+        // columns in order by k_core_sum).
+        double* tc = sm + NW * per_warp;    // [L^2][R]
+        double* u = tc + L2 * R;            // [L][R][R]
+        __syncthreads();
+        for (int e = threadIdx.x; e < L2 * R; e += 128) {
+            const int ij = e / R, r = e % R;
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) s += sm[w * per_warp + T::stage + ij * RP + r];
+            tc[e] = s;
+        }
+        __syncthreads();
+        const double* w1 = a.W1 + cr.c1 * L;
+        for (int e = threadIdx.x; e < L * R * R; e += 128) {
+            const int i = e / (R * R), r1 = (e / R) % R, r2 = e % R;
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < L; ++j) s = fma(__ldg(w1 + (int64_t)r1 * g.n[1] + j), tc[(i * L + j) * R + r2], s);
+            u[e] = s;
+        }
+        __syncthreads();
+        const double* w0 = a.W0 + cr.c0 * L;
+        // Fpart is entry-major, [R^3+1][nblocks], so k_core_sum reads it coalesced
+        const int nblocks = a.S * g.K[0] * g.K[1];
+        double* dst = a.Fpart + (int64_t)cr.seg * g.K[0] * g.K[1] + cr.col;
+        for (int e = threadIdx.x; e < R * R * R; e += 128) {
+            const int r0 = e / (R * R), rr = e % (R * R);
+            double s = 0.0;
+#pragma unroll
+            for (int i = 0; i < L; ++i) s = fma(__ldg(w0 + (int64_t)r0 * g.n[0] + i), u[i * R * R + rr], s);
+            dst[(int64_t)e * nblocks] = s;
+        }
+        __syncthreads();
+        for (int o = 64; o > 0; o >>= 1) {
+            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) dst[(int64_t)R * R * R * nblocks] = red[0];
+        return;
+    }
     if (want_fwd) {
         double* dst = a.T1 + (int64_t)cr.seg * g.n[0] * g.n[1] * R;
         for (int e = threadIdx.x; e < L2 * R; e += 128) {
@@ -566,7 +611,6 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
         }
     }
     if (a.colq) {
-        red[threadIdx.x] = qsum;
         __syncthreads();
         for (int o = 64; o > 0; o >>= 1) {
             if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
@@ -591,13 +635,39 @@ __global__ void __launch_bounds__(256, 3) k_bwd_gather_t(ColumnArgs a, int cells
     double* psi = b2s + L2 * R;   // cells_per_batch x L^3
     __shared__ double lc[16];
     lagrange_consts(L, lc);
-    if (MODE != GATHER_FROM_CELLS)
+    double corr = a.corr ? *a.corr : 0.0;
+    if (MODE != GATHER_FROM_CELLS && a.B2 == nullptr) {
+        // Fused backward y, x expansions (the U_0, U_1 phases of spkmv) for
+        // this column: b2s[(i,j)][r2] = sum_{r0,r1} W0[r0][x_i] W1[r1][y_j] (G .* F)[r0,r1,r2]
+        const int RR = R * R;
+        double* h = psi + (size_t)cells_per_batch * L3;  // [R^3]  G .* F
+        double* v = h + RR * R;                          // [L][R][R]
+        for (int e = tid; e < RR * R; e += 256) h[e] = a.Gc[e] * a.Fc[e];
+        __syncthreads();
+        const double* w0 = a.W0 + cr.c0 * L;
+        for (int e = tid; e < L * RR; e += 256) {
+            const int i = e / RR, rr = e % RR;
+            double s = 0.0;
+            for (int r0 = 0; r0 < R; ++r0) s = fma(__ldg(w0 + (int64_t)r0 * g.n[0] + i), h[r0 * RR + rr], s);
+            v[e] = s;
+        }
+        __syncthreads();
+        const double* w1 = a.W1 + cr.c1 * L;
+        for (int e = tid; e < L2 * R; e += 256) {
+            const int ij = e / R, r2 = e % R, i = ij / L, j = ij % L;
+            double s = 0.0;
+            for (int r1 = 0; r1 < R; ++r1)
+                s = fma(__ldg(w1 + (int64_t)r1 * g.n[1] + j), v[i * RR + r1 * R + r2], s);
+            b2s[e] = s;
+        }
+        corr = a.correction * a.Fc[RR * R];
+    } else if (MODE != GATHER_FROM_CELLS) {
         for (int e = tid; e < L2 * R; e += 256) {
             const int ij = e / R, r = e % R, i = ij / L, j = ij % L;
             b2s[e] = a.B2[((int64_t)(cr.c0 * L + i) * g.n[1] + cr.c1 * L + j) * R + r];
         }
+    }
     const CellAxis ax0 = cell_axis(g, 0, cr.c0), ax1 = cell_axis(g, 1, cr.c1);
-    const double corr = a.corr ? *a.corr : 0.0;
     __syncthreads();
     for (int cb0 = cr.zb; cb0 < cr.ze; cb0 += cells_per_batch) {
         const int cb1 = min(cr.ze, cb0 + cells_per_batch);
@@ -670,7 +740,9 @@ int gather_batch(const Geometry& g) {
 
 template <int L>
 void launch_spread_mma(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
-    const size_t smem = sizeof(double) * SpreadTile<L>::NW * spread_warp_doubles<L>(a.g.R);
+    const int R = a.g.R;
+    const size_t smem = sizeof(double) * (SpreadTile<L>::NW * spread_warp_doubles<L>(R) +
+                                          (size_t)L * L * R + (size_t)L * R * R);
     static int attr_done = 0;
     if (!attr_done) {
         KB_CUDA(cudaFuncSetAttribute(k_spread_mma<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -697,7 +769,9 @@ void launch_gather_t(const ColumnArgs& a, int mode, cudaStream_t s) {
     }
     const int grid = a.g.K[0] * a.g.K[1] * a.S;
     const int cb = gather_batch(a.g);
-    const size_t smem = sizeof(double) * ((size_t)L * L * a.g.R + (size_t)cb * L * L * L);
+    const int R = a.g.R;
+    const size_t smem = sizeof(double) * ((size_t)L * L * R + (size_t)cb * L * L * L +
+                                          (size_t)R * R * R + (size_t)L * R * R);
     switch (mode) {
         case GATHER_FROM_B2:
             k_bwd_gather_t<L, GATHER_FROM_B2><<<grid, 256, smem, s>>>(a, cb);

@@ -49,6 +49,7 @@ struct kpme_gpu_plan_s {
     double* B2 = nullptr;
     double* colq = nullptr;
     double* corr = nullptr;
+    double* Fpart = nullptr;
     // sort
     kb::SortBuffers sb{};
     double4* sp = nullptr;
@@ -163,14 +164,34 @@ kb::ColumnArgs column_args(kpme_gpu_plan p) {
     a.corr = p->corr;
     a.perm = p->sb.perm;
     a.bad = p->sb.bad;
+    a.W0 = p->W[0];
+    a.W1 = p->W[1];
+    a.Gc = p->G;
+    a.correction = p->correction;
     return a;
 }
 
 void sort_and_permute(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q) {
-    kb::launch_sort(p->g, n, xyz, p->sb, p->stream, &p->launches);
-    if (q) {
-        kb::launch_permute(n, xyz, q, p->sb.perm, p->sp, p->stream);
-        if (n > 0) ++p->launches;
+    // the segment sort also writes the sorted particles when q is given
+    kb::launch_sort(p->g, n, xyz, p->sb, p->stream, &p->launches, q, q ? p->sp : nullptr);
+}
+
+// Spread + all forward contractions into core[R^3 + 1]. L <= 8: the DMMA
+// spread emits per-column partial cores, summed in order by k_core_sum;
+// larger L: generic spread to T1 and the separate core kernels.
+void forward_core(kpme_gpu_plan p, kb::ColumnArgs a, double* core) {
+    if (p->g.L <= 8) {
+        a.Fpart = p->Fpart;
+        kb::launch_spread_fwd(a, kb::SPREAD_PARTICLES, true, p->stream);
+        record(p, 2);
+        kb::launch_core_sum(p->g, p->S * p->g.K[0] * p->g.K[1], p->Fpart, core, p->stream);
+        p->launches += 2;
+    } else {
+        kb::launch_spread_fwd(a, kb::SPREAD_PARTICLES, true, p->stream);
+        record(p, 2);
+        kb::launch_core_forward(p->g, p->S, p->T1, p->W[0], p->W[1], p->T2, p->colq, core,
+                                p->stream);
+        p->launches += 3;
     }
 }
 
@@ -200,15 +221,16 @@ void pipeline(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q, do
         p->launches += 4 + 3 * p->nterms;
         return;
     }
-    kb::launch_spread_fwd(a, kb::SPREAD_PARTICLES, true, p->stream);
-    record(p, 2);
-    kb::launch_core_forward(p->g, p->S, p->T1, p->W[0], p->W[1], p->T2, p->colq, p->F, p->stream);
-    kb::launch_core_backward(p->g, p->G, p->F, p->correction, p->W[0], p->W[1], p->B2, p->corr,
-                             p->stream);
+    // spread + z, y, x forward contractions -> one partial core per column
+    forward_core(p, a, p->F);
     record(p, 3);
+    // backward x, y, z expansions + gather - c sum(q), B2 rebuilt per column
+    a.B2 = nullptr;
+    a.Fc = p->F;
+    a.corr = nullptr;
     kb::launch_bwd_gather(a, kb::GATHER_FROM_B2, p->stream);
     record(p, 4);
-    p->launches += 5;
+    p->launches += 1;
 }
 
 // First half for slab plans: sort .. forward contractions into core.
@@ -220,19 +242,18 @@ void forward_half(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q
     reset_flags(p);
     sort_and_permute(p, n, xyz, q);
     kb::ColumnArgs a = column_args(p);
-    kb::launch_spread_fwd(a, kb::SPREAD_PARTICLES, true, p->stream);
-    kb::launch_core_forward(p->g, p->S, p->T1, p->W[0], p->W[1], p->T2, p->colq, core, p->stream);
+    forward_core(p, a, core);
     p->last_n = n;
-    p->launches += 3;
 }
 
 void backward_half(kpme_gpu_plan p, const double* core, double* out) {
-    kb::launch_core_backward(p->g, p->G, core, p->correction, p->W[0], p->W[1], p->B2, p->corr,
-                             p->stream);
     kb::ColumnArgs a = column_args(p);
     a.out = out;
+    a.B2 = nullptr;
+    a.Fc = core;
+    a.corr = nullptr;
     kb::launch_bwd_gather(a, kb::GATHER_FROM_B2, p->stream);
-    p->launches += 2;
+    p->launches += 1;
 }
 
 void collect_times(kpme_gpu_plan p) {
@@ -349,6 +370,7 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, in
             p->F = p->alloc<double>((size_t)R * R * R + 1);
             p->B2 = p->alloc<double>((size_t)g.n[0] * g.n[1] * R);
             p->colq = p->alloc<double>((size_t)p->S * ncol);
+            p->Fpart = p->alloc<double>((size_t)p->S * ncol * ((size_t)R * R * R + 1));
             p->corr = p->alloc<double>(1);
             p->sb.cnt = p->alloc<int32_t>(g.ncell);
             p->sb.start = p->alloc<int32_t>(g.ncell + 1);

@@ -109,11 +109,19 @@ __global__ void k_place(int64_t n, const int32_t* __restrict__ key,
         perm[start[key[i]] + rank[i]] = (int32_t)i;
 }
 
+// sorted particle record for slot s (fused permute)
+__device__ __forceinline__ void put_sp(double4* sp, const double* __restrict__ xyz,
+                                       const double* __restrict__ q, int64_t slot, int32_t v) {
+    if (sp) sp[slot] = make_double4(xyz[3 * (int64_t)v], xyz[3 * (int64_t)v + 1],
+                                    xyz[3 * (int64_t)v + 2], q[v]);
+}
+
 // Warp rank sort of b[0..cnt) (distinct values, padded to P4 with INT_MAX):
 // member k of lane l goes to out[number of smaller members].
 template <int V>
 __device__ __forceinline__ void rank_sort(const int32_t* b, int P4, int cnt, int lane,
-                                          int32_t* out) {
+                                          int32_t* out, double4* sp, const double* xyz,
+                                          const double* q) {
     int v[V], r[V];
 #pragma unroll
     for (int k = 0; k < V; ++k) {
@@ -127,20 +135,30 @@ __device__ __forceinline__ void rank_sort(const int32_t* b, int P4, int cnt, int
     }
 #pragma unroll
     for (int k = 0; k < V; ++k)
-        if (lane + 32 * k < cnt) out[r[k]] = v[k];
+        if (lane + 32 * k < cnt) {
+            out[r[k]] = v[k];
+            put_sp(sp, xyz, q, r[k], v[k]);
+        }
 }
 
 // One warp per cell: restore ascending member order.
 __global__ void __launch_bounds__(256) k_segsort_warp(int ncell, const int32_t* __restrict__ start,
                                                       int32_t* __restrict__ perm,
                                                       int32_t* __restrict__ big,
-                                                      int32_t* __restrict__ nbig) {
+                                                      int32_t* __restrict__ nbig,
+                                                      const double* __restrict__ xyz,
+                                                      const double* __restrict__ q,
+                                                      double4* __restrict__ sp) {
     __shared__ __align__(16) int32_t buf[8][kWarpCap];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cell = blockIdx.x * 8 + w;
     if (cell >= ncell) return;
     const int s0 = start[cell], cnt = start[cell + 1] - s0;
-    if (cnt <= 1) return;
+    if (cnt == 0) return;
+    if (cnt == 1) {
+        if (lane == 0) put_sp(sp, xyz, q, s0, perm[s0]);
+        return;
+    }
     if (cnt > kWarpCap) {
         if (lane == 0) big[atomicAdd(nbig, 1)] = cell;
         return;
@@ -153,7 +171,10 @@ __global__ void __launch_bounds__(256) k_segsort_warp(int ncell, const int32_t* 
                 const bool up = (lane & k) == 0, lower = (lane & j) == 0;
                 v = (lower == up) ? min(v, o) : max(v, o);
             }
-        if (lane < cnt) perm[s0 + lane] = v;
+        if (lane < cnt) {
+            perm[s0 + lane] = v;
+            put_sp(sp, xyz, q, s0 + lane, v);
+        }
         return;
     }
     int32_t* b = buf[w];
@@ -162,8 +183,9 @@ __global__ void __launch_bounds__(256) k_segsort_warp(int ncell, const int32_t* 
         const int P4 = (cnt + 3) & ~3;
         for (int i = lane; i < P4; i += 32) b[i] = i < cnt ? perm[s0 + i] : INT_MAX;
         __syncwarp();
-        if (cnt <= 128) rank_sort<4>(b, P4, cnt, lane, perm + s0);
-        else rank_sort<8>(b, P4, cnt, lane, perm + s0);
+        double4* sps = sp ? sp + s0 : nullptr;
+        if (cnt <= 128) rank_sort<4>(b, P4, cnt, lane, perm + s0, sps, xyz, q);
+        else rank_sort<8>(b, P4, cnt, lane, perm + s0, sps, xyz, q);
         return;
     }
     int P = 512;
@@ -185,7 +207,10 @@ __global__ void __launch_bounds__(256) k_segsort_warp(int ncell, const int32_t* 
             }
             __syncwarp();
         }
-    for (int i = lane; i < cnt; i += 32) perm[s0 + i] = b[i];
+    for (int i = lane; i < cnt; i += 32) {
+        perm[s0 + i] = b[i];
+        put_sp(sp, xyz, q, s0 + i, b[i]);
+    }
 }
 
 // Large cells: one CTA per cell. Up to kBlockCap members are sorted in shared
@@ -195,7 +220,10 @@ __global__ void __launch_bounds__(1024) k_segsort_big(int64_t n, const int32_t* 
                                                       const int32_t* __restrict__ start,
                                                       int32_t* __restrict__ perm,
                                                       const int32_t* __restrict__ big,
-                                                      const int32_t* __restrict__ nbig) {
+                                                      const int32_t* __restrict__ nbig,
+                                                      const double* __restrict__ xyz,
+                                                      const double* __restrict__ q,
+                                                      double4* __restrict__ sp) {
     extern __shared__ int32_t sbuf[];
     __shared__ int32_t wcount[32];
     __shared__ int32_t offset;
@@ -224,7 +252,10 @@ __global__ void __launch_bounds__(1024) k_segsort_big(int64_t n, const int32_t* 
                     }
                     __syncthreads();
                 }
-            for (int i = tid; i < cnt; i += T) perm[s0 + i] = sbuf[i];
+            for (int i = tid; i < cnt; i += T) {
+                perm[s0 + i] = sbuf[i];
+                put_sp(sp, xyz, q, s0 + i, sbuf[i]);
+            }
             __syncthreads();
         } else {
             if (tid == 0) offset = 0;
@@ -244,6 +275,11 @@ __global__ void __launch_bounds__(1024) k_segsort_big(int64_t n, const int32_t* 
                     for (int k = 0; k < (T >> 5); ++k) tot += wcount[k];
                     offset += tot;
                 }
+                __syncthreads();
+            }
+            if (sp) {
+                __threadfence_block();
+                for (int i = tid; i < cnt; i += T) put_sp(sp, xyz, q, s0 + i, perm[s0 + i]);
                 __syncthreads();
             }
         }
@@ -267,7 +303,8 @@ int grid_for(int64_t n, int threads) {
 }  // namespace
 
 void launch_sort(const Geometry& g, int64_t n, const double* xyz, const SortBuffers& b,
-                 cudaStream_t s, int* launches) {
+                 cudaStream_t s, int* launches, const double* q, double4* sp) {
+    if (!q) sp = nullptr;
     static bool attr_set = false;
     if (!attr_set) {
         KB_CUDA(cudaFuncSetAttribute(k_segsort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -288,10 +325,11 @@ void launch_sort(const Geometry& g, int64_t n, const double* xyz, const SortBuff
     if (n > 0) {
         k_place<<<grid_for(n, 256), 256, 0, s>>>(n, b.key, b.rank, b.start, b.perm);
         KB_CHECK_LAUNCH();
-        k_segsort_warp<<<(g.ncell + 7) / 8, 256, 0, s>>>(g.ncell, b.start, b.perm, b.big, b.nbig);
+        k_segsort_warp<<<(g.ncell + 7) / 8, 256, 0, s>>>(g.ncell, b.start, b.perm, b.big, b.nbig,
+                                                         xyz, q, sp);
         KB_CHECK_LAUNCH();
         k_segsort_big<<<148, 1024, kBlockCap * sizeof(int32_t), s>>>(n, b.key, b.start, b.perm,
-                                                                    b.big, b.nbig);
+                                                                    b.big, b.nbig, xyz, q, sp);
         KB_CHECK_LAUNCH();
         l += 4;
     }

@@ -41,6 +41,7 @@ struct Geometry {
     int R;         // compacted Fourier rows per axis, 2M+1 (the m=0 sine row is 0)
     int ncell;     // K0*K1*K2
     int z_lo, z_hi;  // cell planes along axis 2 owned by this plan (slab)
+    double inv_diam; // RN(1 / (2 radius)), for the correctly rounded key division
 };
 
 // ---- sort.cu ----------------------------------------------------------------
@@ -50,6 +51,7 @@ struct SortBuffers {
     int32_t* key;         // [n]
     int32_t* rank;        // [n] provisional slot within the cell
     int32_t* perm;        // [n]
+    double4* rec;         // [n] particle records at their provisional slots
     int32_t* big;         // [ncell] cells too large for the warp sorter
     int32_t* nbig;        // [1]
     unsigned long long* bad;  // [2]: lowest out-of-box index, out-of-cell flag

@@ -24,10 +24,13 @@ __device__ __forceinline__ double cell_hi(const Geometry& g, int a, int i) {
     return g.center[a] - g.radius + 2.0 * g.radius * (i + 1) / g.K[a];
 }
 
-// Same exact key arithmetic as sort.cu (geometry.hpp:141-148).
-__device__ __forceinline__ int axis_cell(double p, double c, double r, int K) {
-    const double t = __ddiv_rn(__dmul_rn(__dsub_rn(p, __dsub_rn(c, r)), (double)K),
-                               __dmul_rn(2.0, r));
+// Same exact key arithmetic as sort.cu (geometry.hpp:141-148), with the
+// correctly rounded (Markstein) division by 2r.
+__device__ __forceinline__ int axis_cell(double p, double c, double r, int K, double y) {
+    const double b = __dmul_rn(2.0, r);
+    const double a = __dmul_rn(__dsub_rn(p, __dsub_rn(c, r)), (double)K);
+    const double q0 = __dmul_rn(a, y);
+    const double t = __fma_rn(__fma_rn(-q0, b, a), y, q0);
     int idx = (int)floor(t);
     if (t == (double)idx && idx > 0) --idx;
     return idx < 0 ? 0 : (idx > K - 1 ? K - 1 : idx);
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(kThreads) k_bwd_gather(ColumnArgs a, int cells
             const int s0 = a.start[cell0], s1 = a.start[cell0 + (cb1 - cb0)];
             for (int s = s0 + tid; s < s1; s += kThreads) {
                 const double4 p = a.sp[s];
-                const int c2 = axis_cell(p.z, g.center[2], g.radius, g.K[2]);
+                const int c2 = axis_cell(p.z, g.center[2], g.radius, g.K[2], g.inv_diam);
                 const double* ps = psi + (c2 - cb0) * L3;
                 double w0[kMaxL], w1[kMaxL], w2[kMaxL];
                 lagrange(g, lc, lo0, hi0, p.x, w0, a.bad);
@@ -625,7 +628,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
 // z = sum_i w0[i] sum_j w1[j] sum_k w2[k] psi[i][j][k] - c_Lambda sum(q),
 // scattered straight to global particle order.
 template <int L, int MODE>
-__global__ void __launch_bounds__(256, 3) k_bwd_gather_t(ColumnArgs a, int cells_per_batch) {
+__global__ void __launch_bounds__(256, 2) k_bwd_gather_t(ColumnArgs a, int cells_per_batch) {
     constexpr int L2 = L * L, L3 = L2 * L;
     const Geometry& g = a.g;
     const int R = g.R, tid = threadIdx.x;
@@ -642,22 +645,24 @@ __global__ void __launch_bounds__(256, 3) k_bwd_gather_t(ColumnArgs a, int cells
         const int RR = R * R;
         double* h = psi + (size_t)cells_per_batch * L3;  // [R^3]  G .* F
         double* v = h + RR * R;                          // [L][R][R]
+        double* w01 = v + L * RR;                        // [2][R][L] W0, W1 column rows
         for (int e = tid; e < RR * R; e += 256) h[e] = a.Gc[e] * a.Fc[e];
+        for (int e = tid; e < R * L; e += 256) {
+            w01[e] = a.W0[(int64_t)(e / L) * g.n[0] + cr.c0 * L + e % L];
+            w01[R * L + e] = a.W1[(int64_t)(e / L) * g.n[1] + cr.c1 * L + e % L];
+        }
         __syncthreads();
-        const double* w0 = a.W0 + cr.c0 * L;
         for (int e = tid; e < L * RR; e += 256) {
             const int i = e / RR, rr = e % RR;
             double s = 0.0;
-            for (int r0 = 0; r0 < R; ++r0) s = fma(__ldg(w0 + (int64_t)r0 * g.n[0] + i), h[r0 * RR + rr], s);
+            for (int r0 = 0; r0 < R; ++r0) s = fma(w01[r0 * L + i], h[r0 * RR + rr], s);
             v[e] = s;
         }
         __syncthreads();
-        const double* w1 = a.W1 + cr.c1 * L;
         for (int e = tid; e < L2 * R; e += 256) {
             const int ij = e / R, r2 = e % R, i = ij / L, j = ij % L;
             double s = 0.0;
-            for (int r1 = 0; r1 < R; ++r1)
-                s = fma(__ldg(w1 + (int64_t)r1 * g.n[1] + j), v[i * RR + r1 * R + r2], s);
+            for (int r1 = 0; r1 < R; ++r1) s = fma(w01[R * L + r1 * L + j], v[i * RR + r1 * R + r2], s);
             b2s[e] = s;
         }
         corr = a.correction * a.Fc[RR * R];
@@ -669,18 +674,26 @@ __global__ void __launch_bounds__(256, 3) k_bwd_gather_t(ColumnArgs a, int cells
     }
     const CellAxis ax0 = cell_axis(g, 0, cr.c0), ax1 = cell_axis(g, 1, cr.c1);
     __syncthreads();
+    double* w2s = psi + (size_t)cells_per_batch * L3 + (size_t)R * R * R + (size_t)L * R * R +
+                  2 * (size_t)R * L;  // [R][cells_per_batch * L] W2 slice of the batch
     for (int cb0 = cr.zb; cb0 < cr.ze; cb0 += cells_per_batch) {
         const int cb1 = min(cr.ze, cb0 + cells_per_batch);
         const int cell0 = (cr.c0 * g.K[1] + cr.c1) * g.K[2] + cb0;
+        const int nz = (cb1 - cb0) * L;
+        if (MODE != GATHER_FROM_CELLS) {
+            for (int e = tid; e < R * nz; e += 256)
+                w2s[e] = a.W2[(int64_t)(e / nz) * g.n[2] + cb0 * L + e % nz];
+            __syncthreads();
+        }
         for (int e = tid; e < (cb1 - cb0) * L3; e += 256) {
-            const int b = e / L3, node = e % L3, c2 = cb0 + b;
+            const int b = e / L3, node = e % L3;
             if (MODE == GATHER_FROM_CELLS) {
                 psi[e] = a.psi_cells[(int64_t)(cell0 + b) * L3 + node];
             } else {
                 const int ij = node / L, k = node % L;
-                const double* wr = a.W2 + c2 * L + k;
+                const double* wr = w2s + b * L + k;
                 double s = 0.0;
-                for (int r = 0; r < R; ++r) s = fma(__ldg(wr + (int64_t)r * g.n[2]), b2s[ij * R + r], s);
+                for (int r = 0; r < R; ++r) s = fma(wr[r * nz], b2s[ij * R + r], s);
                 psi[e] = s;
                 if (a.psi_cells) a.psi_cells[(int64_t)(cell0 + b) * L3 + node] = s;
             }
@@ -697,27 +710,30 @@ __global__ void __launch_bounds__(256, 3) k_bwd_gather_t(ColumnArgs a, int cells
                     pn = a.sp[s + 256];
                     dn = a.perm[s + 256];
                 }
-                const int c2 = axis_cell(p.z, g.center[2], g.radius, g.K[2]);
+                const int c2 = axis_cell(p.z, g.center[2], g.radius, g.K[2], g.inv_diam);
                 const double* ps = psi + (c2 - cb0) * L3;
                 double w0[L], w1[L], w2[L];
                 const CellAxis ax2 = cell_axis(g, 2, c2);
                 lagrange_fast<L>(lc, ax0.lo, ax0.hi, ax0.mid, ax0.inv, p.x, w0, a.bad);
                 lagrange_fast<L>(lc, ax1.lo, ax1.hi, ax1.mid, ax1.inv, p.y, w1, a.bad);
                 lagrange_fast<L>(lc, ax2.lo, ax2.hi, ax2.mid, ax2.inv, p.z, w2, a.bad);
-                double z = 0.0;
+                // z = sum_k w2[k] sum_(i,j) (w0[i] w1[j]) psi[i][j][k]: L independent
+                // accumulators over the L^2 rows of psi (broadcast shared reads)
+                double acc[L];
 #pragma unroll
-                for (int i = 0; i < L; ++i) {
-                    double zi = 0.0;
+                for (int k = 0; k < L; ++k) acc[k] = 0.0;
+#pragma unroll
+                for (int i = 0; i < L; ++i)
 #pragma unroll
                     for (int j = 0; j < L; ++j) {
+                        const double t = w0[i] * w1[j];
                         const double* row = ps + (i * L + j) * L;
-                        double zij = 0.0;
 #pragma unroll
-                        for (int k = 0; k < L; ++k) zij = fma(w2[k], row[k], zij);
-                        zi = fma(w1[j], zij, zi);
+                        for (int k = 0; k < L; ++k) acc[k] = fma(t, row[k], acc[k]);
                     }
-                    z = fma(w0[i], zi, z);
-                }
+                double z = 0.0;
+#pragma unroll
+                for (int k = 0; k < L; ++k) z = fma(w2[k], acc[k], z);
                 a.out[dst] = z - corr;
             }
         }
@@ -771,7 +787,8 @@ void launch_gather_t(const ColumnArgs& a, int mode, cudaStream_t s) {
     const int cb = gather_batch(a.g);
     const int R = a.g.R;
     const size_t smem = sizeof(double) * ((size_t)L * L * R + (size_t)cb * L * L * L +
-                                          (size_t)R * R * R + (size_t)L * R * R);
+                                          (size_t)R * R * R + (size_t)L * R * R +
+                                          2 * (size_t)R * L + (size_t)R * cb * L);
     switch (mode) {
         case GATHER_FROM_B2:
             k_bwd_gather_t<L, GATHER_FROM_B2><<<grid, 256, smem, s>>>(a, cb);

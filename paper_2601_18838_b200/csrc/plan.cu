@@ -334,6 +334,7 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, in
                 g.n[a] = cfg->counts[a] * cfg->order;
             }
             g.radius = cfg->radius;
+            g.inv_diam = 1.0 / (2.0 * cfg->radius);
             g.L = cfg->order;
             g.M = cfg->modes;
             g.R = 2 * cfg->modes + 1;
@@ -376,6 +377,7 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, in
             p->sb.start = p->alloc<int32_t>(g.ncell + 1);
             p->sb.key = p->alloc<int32_t>(p->cap);
             p->sb.rank = p->alloc<int32_t>(p->cap);
+            p->sb.rec = p->alloc<double4>(p->cap);
             p->sb.perm = p->alloc<int32_t>(p->cap);
             p->sb.big = p->alloc<int32_t>(g.ncell);
             p->sb.nbig = p->alloc<int32_t>(1);

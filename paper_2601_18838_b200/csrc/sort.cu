@@ -1,10 +1,16 @@
-// sort.cu -- bit-exact cell sort (assign_particles, geometry.hpp:131-154).
+// sort.cu -- bit-exact cell sort (assign_particles, geometry.hpp:131-154)
+// fused with the construction of the cell-ordered particle records.
 //
-// Pipeline: cell key + box check + histogram whose atomic also hands each
-// particle a provisional slot in its cell (integer atomics only) -> exclusive
-// scan -> placement into cell segments -> per-cell sort of the member indices. The last step restores the reference's "ascending particle
-// index within each cell" order (Partition.members, geometry.hpp:124-127), so
-// the result is identical to the reference whatever order the atomics ran in.
+//   k_keys    cell key in the reference's exact arithmetic + box check; the
+//             histogram atomic also hands out a provisional slot in the cell
+//   k_scan    exclusive scan of the histogram -> cell_start
+//   k_place   perm[start + slot] = i and, with charges, the packed record
+//             (x, y, z, q) at the same provisional slot (coalesced reads,
+//             one 32-byte sector written per particle)
+//   k_segsort per cell: restore the reference's ascending-index member order
+//             (Partition.members, geometry.hpp:124-127) and move the records
+//             inside the cell's contiguous segment
+// The result is identical to the reference whatever order the atomics ran in.
 #include <climits>
 
 #include "internal.h"
@@ -12,15 +18,21 @@
 namespace kb {
 namespace {
 
-constexpr int kWarpCap = 1024;      // largest segment sorted by one warp
-constexpr int kBlockCap = 16384;    // largest segment sorted by one CTA in smem
+constexpr int kRankCap = 256;      // warp rank-count sort
+constexpr int kWarpCap = 512;      // warp bitonic sort of (index, slot) pairs
+constexpr int kBlockCap = 16384;   // CTA bitonic sort in shared memory
 
-// Cell index along one axis, in the reference's exact operation order
-// (geometry.hpp:141-148). Explicit round-to-nearest intrinsics: no FMA
-// contraction may change a bit of t.
-__device__ __forceinline__ int axis_cell(double p, double c, double r, int K) {
-    const double t = __ddiv_rn(__dmul_rn(__dsub_rn(p, __dsub_rn(c, r)), (double)K),
-                               __dmul_rn(2.0, r));
+// Cell index along one axis, bit-identical to the reference
+// (geometry.hpp:141-148): t = ((p - (c - r)) * K) / (2 r), floor, face
+// tie-break, clamp. The division is Markstein's correctly rounded quotient
+// q = RN(q0 + (a - b q0) y) with y = RN(1/b), q0 = RN(a y) (exact FMA
+// remainder), equal to RN(a / b) for these normal operands; the other
+// operations are explicit round-to-nearest (no FMA contraction).
+__device__ __forceinline__ int axis_cell(double p, double c, double r, int K, double b,
+                                         double y) {
+    const double a = __dmul_rn(__dsub_rn(p, __dsub_rn(c, r)), (double)K);
+    const double q0 = __dmul_rn(a, y);
+    const double t = __fma_rn(__fma_rn(-q0, b, a), y, q0);
     int idx = (int)floor(t);
     if (t == (double)idx && idx > 0) --idx;
     if (idx < 0) idx = 0;
@@ -28,100 +40,103 @@ __device__ __forceinline__ int axis_cell(double p, double c, double r, int K) {
     return idx;
 }
 
-__global__ void k_keys(Geometry g, int64_t n, const double* __restrict__ xyz,
-                       int32_t* __restrict__ key, int32_t* __restrict__ rank,
-                       int32_t* __restrict__ cnt, unsigned long long* bad) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const double p0 = xyz[3 * i], p1 = xyz[3 * i + 1], p2 = xyz[3 * i + 2];
-        // Box3::contains (geometry.hpp:36-40)
-        if (fabs(p0 - g.center[0]) > g.radius || fabs(p1 - g.center[1]) > g.radius ||
-            fabs(p2 - g.center[2]) > g.radius)
-            atomicMin(&bad[0], (unsigned long long)i);
-        const int c0 = axis_cell(p0, g.center[0], g.radius, g.K[0]);
-        const int c1 = axis_cell(p1, g.center[1], g.radius, g.K[1]);
-        const int c2 = axis_cell(p2, g.center[2], g.radius, g.K[2]);
-        if (c2 < g.z_lo || c2 >= g.z_hi) atomicOr(&bad[1], 2ull);  // not in this slab
-        const int k = (c0 * g.K[1] + c1) * g.K[2] + c2;  // CellGrid::flatten
-        key[i] = k;
-        rank[i] = atomicAdd(&cnt[k], 1);  // provisional slot, fixed up by k_segsort
-    }
+__global__ void __launch_bounds__(256) k_keys(Geometry g, int64_t n, const double* __restrict__ xyz,
+                                              int32_t* __restrict__ key, int32_t* __restrict__ rank,
+                                              int32_t* __restrict__ cnt, unsigned long long* bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double p0 = xyz[3 * i], p1 = xyz[3 * i + 1], p2 = xyz[3 * i + 2];
+    // Box3::contains (geometry.hpp:36-40)
+    if (fabs(p0 - g.center[0]) > g.radius || fabs(p1 - g.center[1]) > g.radius ||
+        fabs(p2 - g.center[2]) > g.radius)
+        atomicMin(&bad[0], (unsigned long long)i);
+    const double b = __dmul_rn(2.0, g.radius), y = g.inv_diam;
+    const int c0 = axis_cell(p0, g.center[0], g.radius, g.K[0], b, y);
+    const int c1 = axis_cell(p1, g.center[1], g.radius, g.K[1], b, y);
+    const int c2 = axis_cell(p2, g.center[2], g.radius, g.K[2], b, y);
+    if (c2 < g.z_lo || c2 >= g.z_hi) atomicOr(&bad[1], 2ull);  // not in this slab
+    const int k = (c0 * g.K[1] + c1) * g.K[2] + c2;             // CellGrid::flatten
+    key[i] = k;
+    rank[i] = atomicAdd(&cnt[k], 1);  // provisional slot, fixed up by k_segsort
 }
 
-// Exclusive scan of the histogram by one CTA, in shared-memory chunks of
-// kScanChunk counts (coalesced loads, all in flight); leaves start[] and
-// resets cnt[] to the running cursor.
+// Exclusive scan of the histogram by one CTA: chunks of kScanChunk counts,
+// each warp scanning 512 consecutive counts 32 at a time with shuffles.
 constexpr int kScanChunk = 16384;
-__global__ void __launch_bounds__(1024) k_scan(int ncell, int32_t* __restrict__ cnt,
+__global__ void __launch_bounds__(1024) k_scan(int ncell, const int32_t* __restrict__ cnt,
                                                int32_t* __restrict__ start) {
-    extern __shared__ int32_t sc[];  // kScanChunk
-    __shared__ int32_t wsum[32];
+    __shared__ int32_t wtot[32];
     __shared__ int32_t carry;
-    const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    constexpr int per = kScanChunk / 1024;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     if (tid == 0) carry = 0;
+    __syncthreads();
     for (int base = 0; base < ncell; base += kScanChunk) {
-        const int m = min(kScanChunk, ncell - base);
-        for (int i = tid; i < kScanChunk; i += T) sc[i] = i < m ? cnt[base + i] : 0;
-        __syncthreads();
-        int local = 0;
+        int vals[16], own[16];
+        int run = 0;
 #pragma unroll
-        for (int k = 0; k < per; ++k) local += sc[tid * per + k];
-        int x = local;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+        for (int k = 0; k < 16; ++k) {
+            const int idx = base + w * 512 + k * 32 + lane;
+            own[k] = idx < ncell ? cnt[idx] : 0;
         }
-        if (lane == 31) wsum[w] = x;
-        __syncthreads();
-        if (w == 0) {
-            int v = lane < (T >> 5) ? wsum[lane] : 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            int v = own[k];
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, v, o);
                 if (lane >= o) v += y;
             }
-            wsum[lane] = v;
+            vals[k] = run + v;  // inclusive within the warp's 512 counts
+            run += __shfl_sync(0xffffffffu, v, 31);
+        }
+        if (lane == 0) wtot[w] = run;
+        __syncthreads();
+        if (w == 0) {
+            int v = wtot[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += y;
+            }
+            wtot[lane] = v;  // inclusive over warps
         }
         __syncthreads();
-        int run = carry + x - local + (w > 0 ? wsum[w - 1] : 0);
+        const int off = carry + (w > 0 ? wtot[w - 1] : 0);
 #pragma unroll
-        for (int k = 0; k < per; ++k) {
-            const int c = sc[tid * per + k];
-            sc[tid * per + k] = run;
-            run += c;
+        for (int k = 0; k < 16; ++k) {
+            const int idx = base + w * 512 + k * 32 + lane;
+            if (idx < ncell) start[idx] = off + vals[k] - own[k];
         }
         __syncthreads();
-        for (int i = tid; i < m; i += T) {
-            start[base + i] = sc[i];
-            cnt[base + i] = sc[i];
-        }
-        if (tid == T - 1) carry = run;
+        if (tid == 0) carry += wtot[31];
         __syncthreads();
     }
     if (tid == 0) start[ncell] = carry;
 }
 
-__global__ void k_place(int64_t n, const int32_t* __restrict__ key,
-                        const int32_t* __restrict__ rank, const int32_t* __restrict__ start,
-                        int32_t* __restrict__ perm) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        perm[start[key[i]] + rank[i]] = (int32_t)i;
+__global__ void __launch_bounds__(256) k_place(int64_t n, const int32_t* __restrict__ key,
+                                               const int32_t* __restrict__ rank,
+                                               const int32_t* __restrict__ start,
+                                               int32_t* __restrict__ perm,
+                                               const double* __restrict__ xyz,
+                                               const double* __restrict__ q,
+                                               double4* __restrict__ rec) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int pos = start[key[i]] + rank[i];
+    perm[pos] = (int32_t)i;
+    if (rec) rec[pos] = make_double4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], q[i]);
 }
 
-// sorted particle record for slot s (fused permute)
-__device__ __forceinline__ void put_sp(double4* sp, const double* __restrict__ xyz,
-                                       const double* __restrict__ q, int64_t slot, int32_t v) {
-    if (sp) sp[slot] = make_double4(xyz[3 * (int64_t)v], xyz[3 * (int64_t)v + 1],
-                                    xyz[3 * (int64_t)v + 2], q[v]);
+// move the record of provisional slot j (within the segment) to sorted slot r
+__device__ __forceinline__ void move_rec(double4* sp, const double4* rec, int s0, int r, int j) {
+    if (sp) sp[s0 + r] = rec[s0 + j];
 }
 
 // Warp rank sort of b[0..cnt) (distinct values, padded to P4 with INT_MAX):
-// member k of lane l goes to out[number of smaller members].
+// member k of lane l (provisional slot l + 32k) goes to slot
+// (number of smaller members).
 template <int V>
-__device__ __forceinline__ void rank_sort(const int32_t* b, int P4, int cnt, int lane,
-                                          int32_t* out, double4* sp, const double* xyz,
-                                          const double* q) {
+__device__ __forceinline__ void rank_sort(const int32_t* b, int P4, int cnt, int lane, int s0,
+                                          int32_t* perm, double4* sp, const double4* rec) {
     int v[V], r[V];
 #pragma unroll
     for (int k = 0; k < V; ++k) {
@@ -136,95 +151,102 @@ __device__ __forceinline__ void rank_sort(const int32_t* b, int P4, int cnt, int
 #pragma unroll
     for (int k = 0; k < V; ++k)
         if (lane + 32 * k < cnt) {
-            out[r[k]] = v[k];
-            put_sp(sp, xyz, q, r[k], v[k]);
+            perm[s0 + r[k]] = v[k];
+            move_rec(sp, rec, s0, r[k], lane + 32 * k);
         }
 }
 
-// One warp per cell: restore ascending member order.
+// One warp per cell.
 __global__ void __launch_bounds__(256) k_segsort_warp(int ncell, const int32_t* __restrict__ start,
                                                       int32_t* __restrict__ perm,
                                                       int32_t* __restrict__ big,
                                                       int32_t* __restrict__ nbig,
-                                                      const double* __restrict__ xyz,
-                                                      const double* __restrict__ q,
+                                                      const double4* __restrict__ rec,
                                                       double4* __restrict__ sp) {
-    __shared__ __align__(16) int32_t buf[8][kWarpCap];
+    __shared__ __align__(16) unsigned long long buf[8][kWarpCap];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cell = blockIdx.x * 8 + w;
     if (cell >= ncell) return;
     const int s0 = start[cell], cnt = start[cell + 1] - s0;
     if (cnt == 0) return;
     if (cnt == 1) {
-        if (lane == 0) put_sp(sp, xyz, q, s0, perm[s0]);
+        if (lane == 0) move_rec(sp, rec, s0, 0, 0);
         return;
     }
     if (cnt > kWarpCap) {
         if (lane == 0) big[atomicAdd(nbig, 1)] = cell;
         return;
     }
-    if (cnt <= 32) {  // register bitonic network across the warp
+    if (cnt <= 32) {  // register bitonic network on (index, slot) pairs
         int v = lane < cnt ? perm[s0 + lane] : INT_MAX;
+        int j = lane;
         for (int k = 2; k <= 32; k <<= 1)
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                const int o = __shfl_xor_sync(0xffffffffu, v, j);
-                const bool up = (lane & k) == 0, lower = (lane & j) == 0;
-                v = (lower == up) ? min(v, o) : max(v, o);
+            for (int d = k >> 1; d > 0; d >>= 1) {
+                const int ov = __shfl_xor_sync(0xffffffffu, v, d);
+                const int oj = __shfl_xor_sync(0xffffffffu, j, d);
+                const bool up = (lane & k) == 0, lower = (lane & d) == 0;
+                if ((lower == up) == (ov < v)) {
+                    v = ov;
+                    j = oj;
+                }
             }
         if (lane < cnt) {
             perm[s0 + lane] = v;
-            put_sp(sp, xyz, q, s0 + lane, v);
+            move_rec(sp, rec, s0, lane, j);
         }
         return;
     }
-    int32_t* b = buf[w];
-    if (cnt <= 256) {
-        // rank by counting: each member's slot = number of smaller members
+    if (cnt <= kRankCap) {
+        int32_t* b = reinterpret_cast<int32_t*>(buf[w]);
         const int P4 = (cnt + 3) & ~3;
         for (int i = lane; i < P4; i += 32) b[i] = i < cnt ? perm[s0 + i] : INT_MAX;
         __syncwarp();
-        double4* sps = sp ? sp + s0 : nullptr;
-        if (cnt <= 128) rank_sort<4>(b, P4, cnt, lane, perm + s0, sps, xyz, q);
-        else rank_sort<8>(b, P4, cnt, lane, perm + s0, sps, xyz, q);
+        if (cnt <= 128) rank_sort<4>(b, P4, cnt, lane, s0, perm, sp, rec);
+        else rank_sort<8>(b, P4, cnt, lane, s0, perm, sp, rec);
         return;
     }
+    // (index << 32 | slot) pairs, bitonic in shared memory
+    unsigned long long* b = buf[w];
     int P = 512;
     while (P < cnt) P <<= 1;
-    for (int i = lane; i < P; i += 32) b[i] = i < cnt ? perm[s0 + i] : INT_MAX;
+    for (int i = lane; i < P; i += 32)
+        b[i] = i < cnt ? ((unsigned long long)(unsigned)perm[s0 + i] << 32 | (unsigned)i) : ~0ull;
     __syncwarp();
     for (int k = 2; k <= P; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int d = k >> 1; d > 0; d >>= 1) {
             for (int i = lane; i < P; i += 32) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
+                const int ixd = i ^ d;
+                if (ixd > i) {
                     const bool up = (i & k) == 0;
-                    const int x = b[i], y = b[ixj];
+                    const unsigned long long x = b[i], y = b[ixd];
                     if ((x > y) == up) {
                         b[i] = y;
-                        b[ixj] = x;
+                        b[ixd] = x;
                     }
                 }
             }
             __syncwarp();
         }
     for (int i = lane; i < cnt; i += 32) {
-        perm[s0 + i] = b[i];
-        put_sp(sp, xyz, q, s0 + i, b[i]);
+        perm[s0 + i] = (int32_t)(b[i] >> 32);
+        move_rec(sp, rec, s0, i, (int)(b[i] & 0xffffffffu));
     }
 }
 
-// Large cells: one CTA per cell. Up to kBlockCap members are sorted in shared
-// memory; beyond that the CTA rebuilds the segment by a stable, in-order
-// compaction over all keys (O(n) per huge cell, only for degenerate inputs).
+// Large cells: one CTA per cell. Up to kBlockCap members are sorted as
+// (index, slot) pairs in shared memory; beyond that the CTA rebuilds the
+// segment by a stable, in-order compaction over all keys (O(n) per huge
+// cell, only for degenerate inputs) and gathers the records from the inputs.
 __global__ void __launch_bounds__(1024) k_segsort_big(int64_t n, const int32_t* __restrict__ key,
                                                       const int32_t* __restrict__ start,
                                                       int32_t* __restrict__ perm,
                                                       const int32_t* __restrict__ big,
                                                       const int32_t* __restrict__ nbig,
+                                                      const double4* __restrict__ rec,
+                                                      double4* __restrict__ sp,
                                                       const double* __restrict__ xyz,
-                                                      const double* __restrict__ q,
-                                                      double4* __restrict__ sp) {
-    extern __shared__ int32_t sbuf[];
+                                                      const double* __restrict__ q) {
+    extern __shared__ unsigned long long sbuf[];
     __shared__ int32_t wcount[32];
     __shared__ int32_t offset;
     const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, w = tid >> 5;
@@ -235,26 +257,28 @@ __global__ void __launch_bounds__(1024) k_segsort_big(int64_t n, const int32_t* 
         if (cnt <= kBlockCap) {
             int P = 1;
             while (P < cnt) P <<= 1;
-            for (int i = tid; i < P; i += T) sbuf[i] = i < cnt ? perm[s0 + i] : INT_MAX;
+            for (int i = tid; i < P; i += T)
+                sbuf[i] = i < cnt ? ((unsigned long long)(unsigned)perm[s0 + i] << 32 | (unsigned)i)
+                                  : ~0ull;
             __syncthreads();
             for (int k = 2; k <= P; k <<= 1)
-                for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int d = k >> 1; d > 0; d >>= 1) {
                     for (int i = tid; i < P; i += T) {
-                        const int ixj = i ^ j;
-                        if (ixj > i) {
+                        const int ixd = i ^ d;
+                        if (ixd > i) {
                             const bool up = (i & k) == 0;
-                            const int x = sbuf[i], y = sbuf[ixj];
+                            const unsigned long long x = sbuf[i], y = sbuf[ixd];
                             if ((x > y) == up) {
                                 sbuf[i] = y;
-                                sbuf[ixj] = x;
+                                sbuf[ixd] = x;
                             }
                         }
                     }
                     __syncthreads();
                 }
             for (int i = tid; i < cnt; i += T) {
-                perm[s0 + i] = sbuf[i];
-                put_sp(sp, xyz, q, s0 + i, sbuf[i]);
+                perm[s0 + i] = (int32_t)(sbuf[i] >> 32);
+                move_rec(sp, rec, s0, i, (int)(sbuf[i] & 0xffffffffu));
             }
             __syncthreads();
         } else {
@@ -268,18 +292,18 @@ __global__ void __launch_bounds__(1024) k_segsort_big(int64_t n, const int32_t* 
                 __syncthreads();
                 int before = offset;
                 for (int k = 0; k < w; ++k) before += wcount[k];
-                if (hit) perm[s0 + before + __popc(m & ((1u << lane) - 1))] = (int32_t)i;
+                if (hit) {
+                    const int slot = s0 + before + __popc(m & ((1u << lane) - 1));
+                    perm[slot] = (int32_t)i;
+                    if (sp)
+                        sp[slot] = make_double4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], q[i]);
+                }
                 __syncthreads();
                 if (tid == 0) {
                     int tot = 0;
                     for (int k = 0; k < (T >> 5); ++k) tot += wcount[k];
                     offset += tot;
                 }
-                __syncthreads();
-            }
-            if (sp) {
-                __threadfence_block();
-                for (int i = tid; i < cnt; i += T) put_sp(sp, xyz, q, s0 + i, perm[s0 + i]);
                 __syncthreads();
             }
         }
@@ -295,10 +319,7 @@ __global__ void k_permute(int64_t n, const double* __restrict__ xyz, const doubl
     }
 }
 
-int grid_for(int64_t n, int threads) {
-    const int64_t b = (n + threads - 1) / threads;
-    return (int)(b < 1 ? 1 : (b > 148 * 16 ? 148 * 16 : b));
-}
+int blocks_for(int64_t n, int threads) { return (int)((n + threads - 1) / threads); }
 
 }  // namespace
 
@@ -308,28 +329,27 @@ void launch_sort(const Geometry& g, int64_t n, const double* xyz, const SortBuff
     static bool attr_set = false;
     if (!attr_set) {
         KB_CUDA(cudaFuncSetAttribute(k_segsort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kBlockCap * (int)sizeof(int32_t)));
-        KB_CUDA(cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kScanChunk * (int)sizeof(int32_t)));
+                                     kBlockCap * (int)sizeof(unsigned long long)));
         attr_set = true;
     }
     KB_CUDA(cudaMemsetAsync(b.cnt, 0, sizeof(int32_t) * g.ncell, s));
     KB_CUDA(cudaMemsetAsync(b.nbig, 0, sizeof(int32_t), s));
     if (n > 0) {
-        k_keys<<<grid_for(n, 256), 256, 0, s>>>(g, n, xyz, b.key, b.rank, b.cnt, b.bad);
+        k_keys<<<blocks_for(n, 256), 256, 0, s>>>(g, n, xyz, b.key, b.rank, b.cnt, b.bad);
         KB_CHECK_LAUNCH();
     }
-    k_scan<<<1, 1024, kScanChunk * sizeof(int32_t), s>>>(g.ncell, b.cnt, b.start);
+    k_scan<<<1, 1024, 0, s>>>(g.ncell, b.cnt, b.start);
     KB_CHECK_LAUNCH();
     int l = 2;
     if (n > 0) {
-        k_place<<<grid_for(n, 256), 256, 0, s>>>(n, b.key, b.rank, b.start, b.perm);
+        k_place<<<blocks_for(n, 256), 256, 0, s>>>(n, b.key, b.rank, b.start, b.perm, xyz, q,
+                                                   sp ? b.rec : nullptr);
         KB_CHECK_LAUNCH();
         k_segsort_warp<<<(g.ncell + 7) / 8, 256, 0, s>>>(g.ncell, b.start, b.perm, b.big, b.nbig,
-                                                         xyz, q, sp);
+                                                         b.rec, sp);
         KB_CHECK_LAUNCH();
-        k_segsort_big<<<148, 1024, kBlockCap * sizeof(int32_t), s>>>(n, b.key, b.start, b.perm,
-                                                                    b.big, b.nbig, xyz, q, sp);
+        k_segsort_big<<<148, 1024, kBlockCap * sizeof(unsigned long long), s>>>(
+            n, b.key, b.start, b.perm, b.big, b.nbig, b.rec, sp, xyz, q);
         KB_CHECK_LAUNCH();
         l += 4;
     }
@@ -339,7 +359,8 @@ void launch_sort(const Geometry& g, int64_t n, const double* xyz, const SortBuff
 void launch_permute(int64_t n, const double* xyz, const double* q, const int32_t* perm,
                     double4* sp, cudaStream_t s) {
     if (n <= 0) return;
-    k_permute<<<grid_for(n, 256), 256, 0, s>>>(n, xyz, q, perm, sp);
+    const int64_t blk = (n + 255) / 256;
+    k_permute<<<(int)(blk > 148 * 16 ? 148 * 16 : blk), 256, 0, s>>>(n, xyz, q, perm, sp);
     KB_CHECK_LAUNCH();
 }
 

@@ -113,6 +113,38 @@ def test_sort_large_cells(oracle, n, counts):
     np.testing.assert_array_equal(start.cpu().numpy(), ostart)
 
 
+@pytest.mark.parametrize("center,radius,counts", [((0.11, -0.2, 0.05), 0.37, (7, 13, 5)),
+                                                  ((1.0, 2.0, 3.0), 1.0 / 3.0, (3, 9, 27)),
+                                                  ((-5.5, 0.0, 7.25), 12.345, (43, 11, 17))])
+def test_sort_bit_exact_general_box(oracle, center, radius, counts):
+    """Non-power-of-two box diameters exercise the correctly rounded key
+    division; half the points sit exactly on (or one ulp off) cell faces."""
+    from oracle.binding import make_problem
+
+    rng = np.random.default_rng(11)
+    n = 400_000
+    pos = np.array(center) + radius * rng.uniform(-1, 1, (n, 3))
+    faces = []
+    for a in range(3):
+        k = rng.integers(0, counts[a] + 1, n // 2)
+        faces.append(center[a] - radius + 2.0 * radius * k / counts[a])
+    face = np.stack(faces, axis=1)
+    jitter = rng.integers(-1, 2, (n // 2, 3))
+    face = np.where(jitter == 0, face, np.nextafter(face, face + jitter))
+    pos[: n // 2] = face
+    # keep the reference's Box3::contains (|p - c| <= r) true for every point
+    outside = (np.abs(pos - np.array(center)) > radius).any(axis=1)
+    pos[outside] = np.array(center)
+    pb = make_problem(oracle, n=8, counts=counts, order=3, modes=2, eps=1e-6, center=center,
+                      radius=radius)
+    pb.pos, pb.q = pos, np.ones(n)
+    plan = plan_for(pb, n=n)
+    perm, start = plan.sort(dev(pos))
+    operm, ostart = oracle.assign_particles(center, radius, counts, pos)
+    np.testing.assert_array_equal(start.cpu().numpy(), ostart)
+    np.testing.assert_array_equal(perm.cpu().numpy(), operm)
+
+
 def test_outside_particle_rejected_with_index(oracle):
     from oracle.binding import make_problem
 

@@ -627,8 +627,10 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
 // column's cells in shared memory, then one thread per particle,
 // z = sum_i w0[i] sum_j w1[j] sum_k w2[k] psi[i][j][k] - c_Lambda sum(q),
 // scattered straight to global particle order.
+constexpr int GT = 128;  // gather threads per CTA
+
 template <int L, int MODE>
-__global__ void __launch_bounds__(256, 2) k_bwd_gather_t(ColumnArgs a, int cells_per_batch) {
+__global__ void __launch_bounds__(GT, 512 / GT) k_bwd_gather_t(ColumnArgs a, int cells_per_batch) {
     constexpr int L2 = L * L, L3 = L2 * L;
     const Geometry& g = a.g;
     const int R = g.R, tid = threadIdx.x;
@@ -646,20 +648,20 @@ __global__ void __launch_bounds__(256, 2) k_bwd_gather_t(ColumnArgs a, int cells
         double* h = psi + (size_t)cells_per_batch * L3;  // [R^3]  G .* F
         double* v = h + RR * R;                          // [L][R][R]
         double* w01 = v + L * RR;                        // [2][R][L] W0, W1 column rows
-        for (int e = tid; e < RR * R; e += 256) h[e] = a.Gc[e] * a.Fc[e];
-        for (int e = tid; e < R * L; e += 256) {
+        for (int e = tid; e < RR * R; e += GT) h[e] = a.Gc[e] * a.Fc[e];
+        for (int e = tid; e < R * L; e += GT) {
             w01[e] = a.W0[(int64_t)(e / L) * g.n[0] + cr.c0 * L + e % L];
             w01[R * L + e] = a.W1[(int64_t)(e / L) * g.n[1] + cr.c1 * L + e % L];
         }
         __syncthreads();
-        for (int e = tid; e < L * RR; e += 256) {
+        for (int e = tid; e < L * RR; e += GT) {
             const int i = e / RR, rr = e % RR;
             double s = 0.0;
             for (int r0 = 0; r0 < R; ++r0) s = fma(w01[r0 * L + i], h[r0 * RR + rr], s);
             v[e] = s;
         }
         __syncthreads();
-        for (int e = tid; e < L2 * R; e += 256) {
+        for (int e = tid; e < L2 * R; e += GT) {
             const int ij = e / R, r2 = e % R, i = ij / L, j = ij % L;
             double s = 0.0;
             for (int r1 = 0; r1 < R; ++r1) s = fma(w01[R * L + r1 * L + j], v[i * RR + r1 * R + r2], s);
@@ -667,7 +669,7 @@ __global__ void __launch_bounds__(256, 2) k_bwd_gather_t(ColumnArgs a, int cells
         }
         corr = a.correction * a.Fc[RR * R];
     } else if (MODE != GATHER_FROM_CELLS) {
-        for (int e = tid; e < L2 * R; e += 256) {
+        for (int e = tid; e < L2 * R; e += GT) {
             const int ij = e / R, r = e % R, i = ij / L, j = ij % L;
             b2s[e] = a.B2[((int64_t)(cr.c0 * L + i) * g.n[1] + cr.c1 * L + j) * R + r];
         }
@@ -681,15 +683,56 @@ __global__ void __launch_bounds__(256, 2) k_bwd_gather_t(ColumnArgs a, int cells
         const int cell0 = (cr.c0 * g.K[1] + cr.c1) * g.K[2] + cb0;
         const int nz = (cb1 - cb0) * L;
         if (MODE != GATHER_FROM_CELLS) {
-            for (int e = tid; e < R * nz; e += 256)
+            for (int e = tid; e < R * nz; e += GT)
                 w2s[e] = a.W2[(int64_t)(e / nz) * g.n[2] + cb0 * L + e % nz];
             __syncthreads();
         }
-        for (int e = tid; e < (cb1 - cb0) * L3; e += 256) {
-            const int b = e / L3, node = e % L3;
-            if (MODE == GATHER_FROM_CELLS) {
-                psi[e] = a.psi_cells[(int64_t)(cell0 + b) * L3 + node];
-            } else {
+        if (MODE == GATHER_FROM_CELLS) {
+            for (int e = tid; e < (cb1 - cb0) * L3; e += GT)
+                psi[e] = a.psi_cells[(int64_t)(cell0 + (e / L3)) * L3 + e % L3];
+        } else if (L <= 8 && R <= 16) {
+            // psi_cell[(i,j)][k] = sum_r B2col[(i,j)][r] W2[r][c2 L + k]: an
+            // (L^2 x R)(R x L) GEMM per cell on DMMA; the B2col fragments stay
+            // in registers for all cells of the column.
+            constexpr int MT = (L2 + 7) / 8;
+            const int warp = tid >> 5, lane = tid & 31;
+            constexpr int KSMAX = 4;  // R <= 16
+            const int KS = (R + 3) / 4;
+            double af[MT][KSMAX];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int ks = 0; ks < KSMAX; ++ks) {
+                    const int row = mt * 8 + (lane >> 2), r = ks * 4 + (lane & 3);
+                    af[mt][ks] = (ks < KS && row < L2 && r < R) ? b2s[row * R + r] : 0.0;
+                }
+            for (int b = warp; b < cb1 - cb0; b += GT / 32) {
+                double bf[KSMAX];
+#pragma unroll
+                for (int ks = 0; ks < KSMAX; ++ks) {
+                    const int r = ks * 4 + (lane & 3), k = lane >> 2;
+                    bf[ks] = (ks < KS && r < R && k < L) ? w2s[r * nz + b * L + k] : 0.0;
+                }
+                double* ps = psi + b * L3;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    double c[2] = {0.0, 0.0};
+#pragma unroll
+                    for (int ks = 0; ks < KSMAX; ++ks)
+                        if (ks < KS) dmma884(c, af[mt][ks], bf[ks]);
+                    const int row = mt * 8 + (lane >> 2), k0 = 2 * (lane & 3);
+#pragma unroll
+                    for (int cc = 0; cc < 2; ++cc)
+                        if (row < L2 && k0 + cc < L) {
+                            ps[row * L + k0 + cc] = c[cc];
+                            if (a.psi_cells)
+                                a.psi_cells[(int64_t)(cell0 + b) * L3 + row * L + k0 + cc] = c[cc];
+                        }
+                }
+            }
+        } else {
+            for (int e = tid; e < (cb1 - cb0) * L3; e += GT) {
+                const int b = e / L3, node = e % L3;
                 const int ij = node / L, k = node % L;
                 const double* wr = w2s + b * L + k;
                 double s = 0.0;
@@ -703,12 +746,12 @@ __global__ void __launch_bounds__(256, 2) k_bwd_gather_t(ColumnArgs a, int cells
             const int s0 = a.start[cell0], s1 = a.start[cell0 + (cb1 - cb0)];
             double4 pn = s0 + tid < s1 ? a.sp[s0 + tid] : make_double4(0.0, 0.0, 0.0, 0.0);
             int dn = s0 + tid < s1 ? a.perm[s0 + tid] : 0;
-            for (int s = s0 + tid; s < s1; s += 256) {
+            for (int s = s0 + tid; s < s1; s += GT) {
                 const double4 p = pn;  // software prefetch of the next particle
                 const int dst = dn;
-                if (s + 256 < s1) {
-                    pn = a.sp[s + 256];
-                    dn = a.perm[s + 256];
+                if (s + GT < s1) {
+                    pn = a.sp[s + GT];
+                    dn = a.perm[s + GT];
                 }
                 const int c2 = axis_cell(p.z, g.center[2], g.radius, g.K[2], g.inv_diam);
                 const double* ps = psi + (c2 - cb0) * L3;
@@ -749,7 +792,7 @@ size_t spread_smem(const Geometry& g) {
 
 int gather_batch(const Geometry& g) {
     const int L3 = g.L * g.L * g.L;
-    const int cap = (32 * 1024) / (int)(sizeof(double) * L3);
+    const int cap = (24 * 1024) / (int)(sizeof(double) * L3);
     return cap < 1 ? 1 : cap;
 }
 
@@ -791,13 +834,13 @@ void launch_gather_t(const ColumnArgs& a, int mode, cudaStream_t s) {
                                           2 * (size_t)R * L + (size_t)R * cb * L);
     switch (mode) {
         case GATHER_FROM_B2:
-            k_bwd_gather_t<L, GATHER_FROM_B2><<<grid, 256, smem, s>>>(a, cb);
+            k_bwd_gather_t<L, GATHER_FROM_B2><<<grid, GT, smem, s>>>(a, cb);
             break;
         case GATHER_FROM_CELLS:
-            k_bwd_gather_t<L, GATHER_FROM_CELLS><<<grid, 256, smem, s>>>(a, cb);
+            k_bwd_gather_t<L, GATHER_FROM_CELLS><<<grid, GT, smem, s>>>(a, cb);
             break;
         default:
-            k_bwd_gather_t<L, PSI_ONLY><<<grid, 256, smem, s>>>(a, cb);
+            k_bwd_gather_t<L, PSI_ONLY><<<grid, GT, smem, s>>>(a, cb);
     }
     KB_CHECK_LAUNCH();
 }

@@ -191,6 +191,19 @@ __global__ void k_charge_correction(Geometry g, int S, const double* __restrict_
     if (threadIdx.x == 0) *corr = correction * q;
 }
 
+// WL[r][c L + m] = sum_i W[r][c L + i] Lam[i][m]: the factor rows in the
+// monomial basis of each cell (w_i(t) = sum_m Lam[i][m] t^m).
+__global__ void k_factor_wl(Geometry g, int a, const double* __restrict__ W,
+                            const double* __restrict__ lam, double* __restrict__ WL) {
+    const int n = g.n[a], L = g.L;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < g.R * n; e += gridDim.x * blockDim.x) {
+        const int r = e / n, x = e % n, c = x / L, m = x % L;
+        double s = 0.0;
+        for (int i = 0; i < L; ++i) s = fma(W[(int64_t)r * n + c * L + i], lam[i * L + m], s);
+        WL[e] = s;
+    }
+}
+
 // out[t][u][v] = sum_r W[r][u] D[t][a][r] W[r][v]  (dense A_a(lambda))
 __global__ void k_axis_operands(Geometry g, int a, int nterms, const double* __restrict__ W,
                                 const double* __restrict__ D, double* __restrict__ out) {
@@ -275,6 +288,12 @@ void launch_core_sum(const Geometry& g, int nblocks, const double* Fpart, double
 void launch_charge_correction(const Geometry& g, int S, const double* colq, double correction,
                               double* corr, cudaStream_t s) {
     k_charge_correction<<<1, 128, 0, s>>>(g, S, colq, correction, corr);
+    KB_CHECK_LAUNCH();
+}
+
+void launch_factor_wl(const Geometry& g, int axis, const double* W, const double* lam, double* WL,
+                      cudaStream_t s) {
+    k_factor_wl<<<64, 256, 0, s>>>(g, axis, W, lam, WL);
     KB_CHECK_LAUNCH();
 }
 

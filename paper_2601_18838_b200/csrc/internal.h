@@ -87,6 +87,9 @@ struct ColumnArgs {
     const double* Gc;        // [R^3] collapsed SKP core
     const double* Fc;        // [R^3+1] summed core
     double correction;       // c_Lambda
+    // monomial hot path: the W tables above are W_a Lambda (Lagrange basis ->
+    // powers of the cell-local coordinate) and particles carry t^a, not w_k(t)
+    int mono;
 };
 enum SpreadMode { SPREAD_PARTICLES = 0, SPREAD_FROM_CELLS = 1 };
 enum GatherMode { GATHER_FROM_B2 = 0, GATHER_FROM_CELLS = 1, PSI_ONLY = 2 };
@@ -109,6 +112,9 @@ void launch_core_sum(const Geometry& g, int nblocks, const double* Fpart, double
 // corr = correction * sum(colq), columns in order
 void launch_charge_correction(const Geometry& g, int S, const double* colq, double correction,
                               double* corr, cudaStream_t s);
+// WL[r][c L + a] = sum_i W[r][c L + i] Lam[i][a] for one axis
+void launch_factor_wl(const Geometry& g, int axis, const double* W, const double* lam, double* WL,
+                      cudaStream_t s);
 void launch_axis_operands(const Geometry& g, int axis, int nterms, const double* W,
                           const double* D, double* out, cudaStream_t s);
 // inverse == false: src = cells, dst = mesh; inverse == true: src = mesh, dst = cells

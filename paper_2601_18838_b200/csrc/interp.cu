@@ -361,6 +361,19 @@ __device__ __forceinline__ int warp_lower_bound(const int32_t* start, int cb, in
     return ce;
 }
 
+// Powers t^a of the cell-local coordinate t = (y - mid) / half (monomial hot
+// path), with the same out-of-cell check as tensor_weights.
+template <int L>
+__device__ __forceinline__ void powers(double lo, double hi, double mid, double inv_half,
+                                       double y, double (&w)[L], unsigned long long* bad) {
+    const double slack = 1e-12 * (hi - lo);
+    if (y < lo - slack || y > hi + slack) atomicOr(&bad[1], 1ull);
+    const double t = (y - mid) * inv_half;
+    w[0] = 1.0;
+#pragma unroll
+    for (int k = 1; k < L; ++k) w[k] = w[k - 1] * t;
+}
+
 struct CellAxis {
     double lo, hi, mid, inv;
 };
@@ -413,7 +426,7 @@ __device__ __forceinline__ void zero_padding(double* As, double* Bs, int lane) {
     for (int e = lane; e < (T::NT * 8 - T::L2) * T::LDP; e += 32) Bs[T::L2 * T::LDP + e] = 0.0;
 }
 
-template <int L>
+template <int L, bool MONO>
 __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, int want_fwd) {
     using T = SpreadTile<L>;
     constexpr int L2 = T::L2, L3 = L2 * L, NT = T::NT, LDP = T::LDP, NW = T::NW, CH = T::CH;
@@ -474,9 +487,15 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
             double w0[L], w1[L], w2[L];
             const double qv = p < cnt ? pt.w : 0.0;
             qsum += half == 0 ? qv : 0.0;
-            lagrange_fast<L>(lc, ax0.lo, ax0.hi, ax0.mid, ax0.inv, pt.x, w0, a.bad);
-            lagrange_fast<L>(lc, ax1.lo, ax1.hi, ax1.mid, ax1.inv, pt.y, w1, a.bad);
-            lagrange_fast<L>(lc, ax2.lo, ax2.hi, ax2.mid, ax2.inv, pt.z, w2, a.bad);
+            if (MONO) {
+                powers<L>(ax0.lo, ax0.hi, ax0.mid, ax0.inv, pt.x, w0, a.bad);
+                powers<L>(ax1.lo, ax1.hi, ax1.mid, ax1.inv, pt.y, w1, a.bad);
+                powers<L>(ax2.lo, ax2.hi, ax2.mid, ax2.inv, pt.z, w2, a.bad);
+            } else {
+                lagrange_fast<L>(lc, ax0.lo, ax0.hi, ax0.mid, ax0.inv, pt.x, w0, a.bad);
+                lagrange_fast<L>(lc, ax1.lo, ax1.hi, ax1.mid, ax1.inv, pt.y, w1, a.bad);
+                lagrange_fast<L>(lc, ax2.lo, ax2.hi, ax2.mid, ax2.inv, pt.z, w2, a.bad);
+            }
             __syncwarp();
             // lane pair (p, p+16): A rows [4h, 4h+4) and B rows j in [JH h, JH h + JH)
 #pragma unroll
@@ -629,7 +648,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
 // scattered straight to global particle order.
 constexpr int GT = 128;  // gather threads per CTA
 
-template <int L, int MODE>
+template <int L, int MODE, bool MONO>
 __global__ void __launch_bounds__(GT, 512 / GT) k_bwd_gather_t(ColumnArgs a, int cells_per_batch) {
     constexpr int L2 = L * L, L3 = L2 * L;
     const Geometry& g = a.g;
@@ -755,28 +774,55 @@ __global__ void __launch_bounds__(GT, 512 / GT) k_bwd_gather_t(ColumnArgs a, int
                 }
                 const int c2 = axis_cell(p.z, g.center[2], g.radius, g.K[2], g.inv_diam);
                 const double* ps = psi + (c2 - cb0) * L3;
-                double w0[L], w1[L], w2[L];
                 const CellAxis ax2 = cell_axis(g, 2, c2);
-                lagrange_fast<L>(lc, ax0.lo, ax0.hi, ax0.mid, ax0.inv, p.x, w0, a.bad);
-                lagrange_fast<L>(lc, ax1.lo, ax1.hi, ax1.mid, ax1.inv, p.y, w1, a.bad);
-                lagrange_fast<L>(lc, ax2.lo, ax2.hi, ax2.mid, ax2.inv, p.z, w2, a.bad);
-                // z = sum_k w2[k] sum_(i,j) (w0[i] w1[j]) psi[i][j][k]: L independent
-                // accumulators over the L^2 rows of psi (broadcast shared reads)
-                double acc[L];
-#pragma unroll
-                for (int k = 0; k < L; ++k) acc[k] = 0.0;
-#pragma unroll
-                for (int i = 0; i < L; ++i)
-#pragma unroll
-                    for (int j = 0; j < L; ++j) {
-                        const double t = w0[i] * w1[j];
-                        const double* row = ps + (i * L + j) * L;
-#pragma unroll
-                        for (int k = 0; k < L; ++k) acc[k] = fma(t, row[k], acc[k]);
-                    }
                 double z = 0.0;
+                if (MONO) {
+                    // ps = monomial coefficients C[a][b][c] of this cell's potential:
+                    // z = sum_a t0^a sum_b t1^b sum_c t2^c C[a][b][c] (nested Horner)
+                    double t[3];
+                    const CellAxis* axs[3] = {&ax0, &ax1, &ax2};
+                    const double yv[3] = {p.x, p.y, p.z};
 #pragma unroll
-                for (int k = 0; k < L; ++k) z = fma(w2[k], acc[k], z);
+                    for (int d = 0; d < 3; ++d) {
+                        const CellAxis& A = *axs[d];
+                        const double slack = 1e-12 * (A.hi - A.lo);
+                        if (yv[d] < A.lo - slack || yv[d] > A.hi + slack) atomicOr(&a.bad[1], 1ull);
+                        t[d] = (yv[d] - A.mid) * A.inv;
+                    }
+#pragma unroll
+                    for (int i = L - 1; i >= 0; --i) {
+                        double zb = 0.0;
+#pragma unroll
+                        for (int j = L - 1; j >= 0; --j) {
+                            const double* row = ps + (i * L + j) * L;
+                            double zc = row[L - 1];
+#pragma unroll
+                            for (int k = L - 2; k >= 0; --k) zc = fma(zc, t[2], row[k]);
+                            zb = fma(zb, t[1], zc);
+                        }
+                        z = fma(z, t[0], zb);
+                    }
+                } else {
+                    double w0[L], w1[L], w2[L];
+                    lagrange_fast<L>(lc, ax0.lo, ax0.hi, ax0.mid, ax0.inv, p.x, w0, a.bad);
+                    lagrange_fast<L>(lc, ax1.lo, ax1.hi, ax1.mid, ax1.inv, p.y, w1, a.bad);
+                    lagrange_fast<L>(lc, ax2.lo, ax2.hi, ax2.mid, ax2.inv, p.z, w2, a.bad);
+                    // z = sum_k w2[k] sum_(i,j) (w0[i] w1[j]) psi[i][j][k]
+                    double acc[L];
+#pragma unroll
+                    for (int k = 0; k < L; ++k) acc[k] = 0.0;
+#pragma unroll
+                    for (int i = 0; i < L; ++i)
+#pragma unroll
+                        for (int j = 0; j < L; ++j) {
+                            const double tt = w0[i] * w1[j];
+                            const double* row = ps + (i * L + j) * L;
+#pragma unroll
+                            for (int k = 0; k < L; ++k) acc[k] = fma(tt, row[k], acc[k]);
+                        }
+#pragma unroll
+                    for (int k = 0; k < L; ++k) z = fma(w2[k], acc[k], z);
+                }
                 a.out[dst] = z - corr;
             }
         }
@@ -797,35 +843,44 @@ int gather_batch(const Geometry& g) {
 }
 
 
-template <int L>
-void launch_spread_mma(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
+template <int L, bool MONO>
+void launch_spread_mma_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
     const int R = a.g.R;
     const size_t smem = sizeof(double) * (SpreadTile<L>::NW * spread_warp_doubles<L>(R) +
                                           (size_t)L * L * R + (size_t)L * R * R);
     static int attr_done = 0;
     if (!attr_done) {
-        KB_CUDA(cudaFuncSetAttribute(k_spread_mma<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     200 * 1024));
+        KB_CUDA(cudaFuncSetAttribute(k_spread_mma<L, MONO>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr_done = 1;
     }
     if (smem > 200 * 1024) throw Error(KPME_GPU_INVALID_ARGUMENT, "spread: tile too large");
     const int grid = a.g.K[0] * a.g.K[1] * a.S;
-    k_spread_mma<L><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+    k_spread_mma<L, MONO><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
     KB_CHECK_LAUNCH();
 }
 
 template <int L>
-void launch_gather_t(const ColumnArgs& a, int mode, cudaStream_t s) {
+void launch_spread_mma(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
+    if (a.mono)
+        launch_spread_mma_t<L, true>(a, want_fwd, s);
+    else
+        launch_spread_mma_t<L, false>(a, want_fwd, s);
+}
+
+template <int L, int MODE, bool MONO>
+void launch_gather_mode(const ColumnArgs& a, int grid, int cb, size_t smem, cudaStream_t s) {
     static int attr_done = 0;
     if (!attr_done) {
-        KB_CUDA(cudaFuncSetAttribute(k_bwd_gather_t<L, GATHER_FROM_B2>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        KB_CUDA(cudaFuncSetAttribute(k_bwd_gather_t<L, GATHER_FROM_CELLS>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        KB_CUDA(cudaFuncSetAttribute(k_bwd_gather_t<L, PSI_ONLY>,
+        KB_CUDA(cudaFuncSetAttribute(k_bwd_gather_t<L, MODE, MONO>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr_done = 1;
     }
+    k_bwd_gather_t<L, MODE, MONO><<<grid, GT, smem, s>>>(a, cb);
+}
+
+template <int L>
+void launch_gather_t(const ColumnArgs& a, int mode, cudaStream_t s) {
     const int grid = a.g.K[0] * a.g.K[1] * a.S;
     const int cb = gather_batch(a.g);
     const int R = a.g.R;
@@ -834,13 +889,16 @@ void launch_gather_t(const ColumnArgs& a, int mode, cudaStream_t s) {
                                           2 * (size_t)R * L + (size_t)R * cb * L);
     switch (mode) {
         case GATHER_FROM_B2:
-            k_bwd_gather_t<L, GATHER_FROM_B2><<<grid, GT, smem, s>>>(a, cb);
+            if (a.mono && L <= 8)
+                launch_gather_mode<L, GATHER_FROM_B2, true>(a, grid, cb, smem, s);
+            else
+                launch_gather_mode<L, GATHER_FROM_B2, false>(a, grid, cb, smem, s);
             break;
         case GATHER_FROM_CELLS:
-            k_bwd_gather_t<L, GATHER_FROM_CELLS><<<grid, GT, smem, s>>>(a, cb);
+            launch_gather_mode<L, GATHER_FROM_CELLS, false>(a, grid, cb, smem, s);
             break;
         default:
-            k_bwd_gather_t<L, PSI_ONLY><<<grid, GT, smem, s>>>(a, cb);
+            launch_gather_mode<L, PSI_ONLY, false>(a, grid, cb, smem, s);
     }
     KB_CHECK_LAUNCH();
 }

@@ -40,6 +40,8 @@ struct kpme_gpu_plan_s {
     double* tw = nullptr;
     double* prof = nullptr;
     double* W[3] = {nullptr, nullptr, nullptr};
+    double* WL[3] = {nullptr, nullptr, nullptr};  // W_a Lambda (monomial hot path)
+    double* lam = nullptr;
     double* D = nullptr;
     double* G = nullptr;
     // collapsed-core work
@@ -176,12 +178,21 @@ void sort_and_permute(kpme_gpu_plan p, int64_t n, const double* xyz, const doubl
     kb::launch_sort(p->g, n, xyz, p->sb, p->stream, &p->launches, q, q ? p->sp : nullptr);
 }
 
+// Hot path for L <= 8: factor rows in the monomial basis of each cell.
+void mono_tables(kpme_gpu_plan p, kb::ColumnArgs& a) {
+    a.mono = 1;
+    a.W0 = p->WL[0];
+    a.W1 = p->WL[1];
+    a.W2 = p->WL[2];
+}
+
 // Spread + all forward contractions into core[R^3 + 1]. L <= 8: the DMMA
 // spread emits per-column partial cores, summed in order by k_core_sum;
 // larger L: generic spread to T1 and the separate core kernels.
 void forward_core(kpme_gpu_plan p, kb::ColumnArgs a, double* core) {
     if (p->g.L <= 8) {
         a.Fpart = p->Fpart;
+        mono_tables(p, a);
         kb::launch_spread_fwd(a, kb::SPREAD_PARTICLES, true, p->stream);
         record(p, 2);
         kb::launch_core_sum(p->g, p->S * p->g.K[0] * p->g.K[1], p->Fpart, core, p->stream);
@@ -228,6 +239,7 @@ void pipeline(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q, do
     a.B2 = nullptr;
     a.Fc = p->F;
     a.corr = nullptr;
+    if (p->g.L <= 8) mono_tables(p, a);
     kb::launch_bwd_gather(a, kb::GATHER_FROM_B2, p->stream);
     record(p, 4);
     p->launches += 1;
@@ -252,6 +264,7 @@ void backward_half(kpme_gpu_plan p, const double* core, double* out) {
     a.B2 = nullptr;
     a.Fc = core;
     a.corr = nullptr;
+    if (p->g.L <= 8) mono_tables(p, a);
     kb::launch_bwd_gather(a, kb::GATHER_FROM_B2, p->stream);
     p->launches += 1;
 }
@@ -387,6 +400,36 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, in
             KB_CUDA(cudaMemsetAsync(p->colq, 0, sizeof(double) * p->S * ncol, p->stream));
             kb::launch_factor_tables(g, p->nterms, p->tw, p->prof, p->W[0], p->W[1], p->W[2], p->D,
                                      p->G, p->stream);
+            if (L <= 8) {
+                // Lagrange basis -> monomials of the cell-local coordinate:
+                // w_k(t) = c_k prod_{j != k} (t - t_j) = sum_m Lam[k][m] t^m
+                std::vector<double> lam(L * L);
+                for (int k = 0; k < L; ++k) {
+                    std::vector<long double> poly(1, 1.0L);
+                    long double ck = 1.0L;
+                    const long double tk = -1.0L + 2.0L * k / (L - 1);
+                    for (int j = 0; j < L; ++j) {
+                        if (j == k) continue;
+                        const long double tj = -1.0L + 2.0L * j / (L - 1);
+                        ck *= (tk - tj);
+                        std::vector<long double> nxt(poly.size() + 1, 0.0L);
+                        for (size_t m = 0; m < poly.size(); ++m) {
+                            nxt[m + 1] += poly[m];
+                            nxt[m] -= tj * poly[m];
+                        }
+                        poly.swap(nxt);
+                    }
+                    for (int m = 0; m < L; ++m) lam[k * L + m] = (double)(poly[m] / ck);
+                }
+                p->lam = p->alloc<double>(L * L);
+                KB_CUDA(cudaMemcpyAsync(p->lam, lam.data(), sizeof(double) * L * L,
+                                        cudaMemcpyHostToDevice, p->stream));
+                for (int a = 0; a < 3; ++a) {
+                    p->WL[a] = p->alloc<double>((size_t)R * g.n[a]);
+                    kb::launch_factor_wl(g, a, p->W[a], p->lam, p->WL[a], p->stream);
+                }
+                KB_CUDA(cudaStreamSynchronize(p->stream));
+            }
             if (p->form == KPME_GPU_FORM_DENSE) {
                 const size_t cells = (size_t)g.ncell * L * L * L;
                 p->cells = p->alloc<double>(cells);

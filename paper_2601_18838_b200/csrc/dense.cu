@@ -46,11 +46,16 @@ __device__ __forceinline__ void cp_wait() {
 }
 
 // VEC16: all rows 16-byte aligned (M and K even, pointers aligned) -> 16-byte copies.
+// blockIdx.z selects a batch entry: in += z * sin, F += z * sF, out += z * sout.
 template <bool VEC16>
 __global__ void __launch_bounds__(THREADS) k_dgemm_tn(int64_t M, int64_t N, int64_t K,
                                                       const double* __restrict__ in,
                                                       const double* __restrict__ F,
-                                                      double* __restrict__ out, int accumulate) {
+                                                      double* __restrict__ out, int accumulate,
+                                                      int64_t sin, int64_t sF, int64_t sout) {
+    in += blockIdx.z * sin;
+    F += blockIdx.z * sF;
+    out += blockIdx.z * sout;
     extern __shared__ __align__(16) double smem[];
     double* As = smem;                         // [STAGES][BK][LDA]
     double* Bs = smem + STAGES * BK * LDA;     // [STAGES][BN][LDB]
@@ -145,6 +150,17 @@ __global__ void __launch_bounds__(THREADS) k_dgemm_tn(int64_t M, int64_t N, int6
     }
 }
 
+// out[e] (+)= sum_s part[s][e] over splits in order (deterministic split-K).
+__global__ void k_sum_splits(int64_t E, int splits, const double* __restrict__ part,
+                             double* __restrict__ out, int accumulate) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        double s = accumulate ? out[e] : 0.0;
+        for (int k = 0; k < splits; ++k) s += part[(int64_t)k * E + e];
+        out[e] = s;
+    }
+}
+
 // Ccat[z'][r * n2 + z] = C_r[z'][z]: the term-concatenated last-pass operand.
 __global__ void k_concat_terms(int nterms, int n, const double* __restrict__ C,
                                double* __restrict__ Ccat) {
@@ -157,16 +173,35 @@ __global__ void k_concat_terms(int nterms, int n, const double* __restrict__ C,
 }
 
 int chunk_terms(int n0, int n1, int n2, int nterms) {
-    // keep the term-stacked intermediates within ~16 GB of HBM
+    // keep the term-stacked intermediates (two per term) within ~16 GB of HBM
     const double mesh = 8.0 * n0 * n1 * n2;
-    int c = (int)std::max(1.0, std::min((double)nterms, 16e9 / mesh));
+    int c = (int)std::max(1.0, std::min((double)nterms, 8e9 / mesh));
     return std::max(1, std::min(c, nterms));
+}
+
+// CTA tiles of one mode-product GEMM; below ~2 waves the passes are batched
+// over terms and the last pass is split over terms.
+int64_t tiles(int64_t M, int64_t N) { return ((M + BM - 1) / BM) * ((N + BN - 1) / BN); }
+int splits_for(int n0, int n1, int n2, int chunk) {
+    const int64_t t = tiles((int64_t)n0 * n1, n2);
+    int s = (int)std::max<int64_t>(1, (2 * 148 + t - 1) / t);
+    return std::max(1, std::min(s, chunk));
 }
 
 }  // namespace
 
+void dgemm_tn_batched(cudaStream_t s, int64_t M, int64_t N, int64_t K, const double* in,
+                      int64_t sin, const double* F, int64_t sF, double* out, int64_t sout,
+                      int batch, bool accumulate);
+
 void dgemm_tn(cudaStream_t s, int64_t M, int64_t N, int64_t K, const double* in, const double* F,
               double* out, bool accumulate) {
+    dgemm_tn_batched(s, M, N, K, in, 0, F, 0, out, 0, 1, accumulate);
+}
+
+void dgemm_tn_batched(cudaStream_t s, int64_t M, int64_t N, int64_t K, const double* in,
+                      int64_t sin, const double* F, int64_t sF, double* out, int64_t sout,
+                      int batch, bool accumulate) {
     static bool attr = false;
     if (!attr) {
         KB_CUDA(cudaFuncSetAttribute(k_dgemm_tn<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -175,21 +210,24 @@ void dgemm_tn(cudaStream_t s, int64_t M, int64_t N, int64_t K, const double* in,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
         attr = true;
     }
-    if (M <= 0 || N <= 0) return;
-    const dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
+    if (M <= 0 || N <= 0 || batch <= 0) return;
+    const dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)batch);
     const bool vec = (M % 2 == 0) && (K % 2 == 0) && ((uintptr_t)in % 16 == 0) &&
-                     ((uintptr_t)F % 16 == 0);
+                     ((uintptr_t)F % 16 == 0) && (sin % 2 == 0) && (sF % 2 == 0);
     if (vec)
-        k_dgemm_tn<true><<<grid, THREADS, kSmem, s>>>(M, N, K, in, F, out, accumulate ? 1 : 0);
+        k_dgemm_tn<true><<<grid, THREADS, kSmem, s>>>(M, N, K, in, F, out, accumulate ? 1 : 0, sin,
+                                                      sF, sout);
     else
-        k_dgemm_tn<false><<<grid, THREADS, kSmem, s>>>(M, N, K, in, F, out, accumulate ? 1 : 0);
+        k_dgemm_tn<false><<<grid, THREADS, kSmem, s>>>(M, N, K, in, F, out, accumulate ? 1 : 0,
+                                                       sin, sF, sout);
     KB_CHECK_LAUNCH();
 }
 
 size_t dense_workspace_bytes(int n0, int n1, int n2, int nterms) {
     const size_t mesh = (size_t)n0 * n1 * n2;
     const int c = chunk_terms(n0, n1, n2, nterms);
-    return sizeof(double) * (mesh * (1 + (size_t)c) + (size_t)n2 * n2 * c) + 256;
+    const int sp = splits_for(n0, n1, n2, c);
+    return sizeof(double) * (mesh * (2 * (size_t)c + (sp > 1 ? sp : 0)) + (size_t)n2 * n2 * c) + 256;
 }
 
 void kron_matvec_dense(cudaStream_t s, int n0, int n1, int n2, int nterms, const double* A,
@@ -201,25 +239,42 @@ void kron_matvec_dense(cudaStream_t s, int n0, int n1, int n2, int nterms, const
         return;
     }
     const int chunk = chunk_terms(n0, n1, n2, nterms);
+    const int splits = splits_for(n0, n1, n2, chunk);
     if (work_bytes < dense_workspace_bytes(n0, n1, n2, nterms))
         throw Error(KPME_GPU_INVALID_ARGUMENT, "kron_matvec_dense: workspace too small");
-    double* t1 = work;                          // [n1][n2][n0]
-    double* t2 = t1 + mesh;                     // [chunk][n2][n0][n1]
+    double* t1 = work;                          // [chunk][n1][n2][n0]
+    double* t2 = t1 + mesh * chunk;             // [chunk][n2][n0][n1]
     double* ccat = t2 + mesh * chunk;           // [n2][chunk * n2]
+    double* part = ccat + (int64_t)n2 * n2 * chunk;  // [splits][n0 n1][n2]
     for (int r0 = 0; r0 < nterms; r0 += chunk) {
         const int cr = std::min(chunk, nterms - r0);
-        for (int r = 0; r < cr; ++r) {
-            const int t = r0 + r;
-            // pass A: contract x (K = n0): t1[(y,z)][x'] = sum_x x[x][(y,z)] A_t[x'][x]
-            dgemm_tn(s, (int64_t)n1 * n2, n0, n0, x, A + (int64_t)t * n0 * n0, t1, false);
-            // pass B: contract y (K = n1): t2_r[(z,x')][y'] = sum_y t1[y][(z,x')] B_t[y'][y]
-            dgemm_tn(s, (int64_t)n2 * n0, n1, n1, t1, B + (int64_t)t * n1 * n1, t2 + r * mesh,
-                     false);
-        }
+        // pass A, all terms of the chunk in one launch: t1_r = x ^T-contracted with A_r
+        dgemm_tn_batched(s, (int64_t)n1 * n2, n0, n0, x, 0, A + (int64_t)r0 * n0 * n0,
+                         (int64_t)n0 * n0, t1, mesh, cr, false);
+        // pass B: t2_r[(z,x')][y'] = sum_y t1_r[y][(z,x')] B_r[y'][y]
+        dgemm_tn_batched(s, (int64_t)n2 * n0, n1, n1, t1, mesh, B + (int64_t)r0 * n1 * n1,
+                         (int64_t)n1 * n1, t2, mesh, cr, false);
         // pass C over (term, z): y[(x',y')][z'] (+)= sum_{r,z} t2[r][z][(x',y')] C_r[z'][z]
-        k_concat_terms<<<148 * 4, 256, 0, s>>>(cr, n2, C + (int64_t)r0 * n2 * n2, ccat);
-        KB_CHECK_LAUNCH();
-        dgemm_tn(s, (int64_t)n0 * n1, n2, (int64_t)cr * n2, t2, ccat, y, r0 > 0);
+        const int sp = std::min(splits, cr);
+        if (sp <= 1) {
+            k_concat_terms<<<148 * 4, 256, 0, s>>>(cr, n2, C + (int64_t)r0 * n2 * n2, ccat);
+            KB_CHECK_LAUNCH();
+            dgemm_tn(s, (int64_t)n0 * n1, n2, (int64_t)cr * n2, t2, ccat, y, r0 > 0);
+        } else {
+            // split-K over terms: split k covers terms [k*cr/sp, (k+1)*cr/sp), with its own
+            // concatenated operand [z'][(tb-ta) n2] at ccat + ta n2^2
+            for (int k = 0; k < sp; ++k) {
+                const int ta = k * cr / sp, tb = (k + 1) * cr / sp;
+                double* ck = ccat + (int64_t)ta * n2 * n2;
+                k_concat_terms<<<148 * 2, 256, 0, s>>>(tb - ta, n2,
+                                                       C + (int64_t)(r0 + ta) * n2 * n2, ck);
+                KB_CHECK_LAUNCH();
+                dgemm_tn(s, (int64_t)n0 * n1, n2, (int64_t)(tb - ta) * n2, t2 + ta * mesh, ck,
+                         part + k * mesh, false);
+            }
+            k_sum_splits<<<148 * 8, 256, 0, s>>>(mesh, sp, part, y, r0 > 0 ? 1 : 0);
+            KB_CHECK_LAUNCH();
+        }
     }
 }
 

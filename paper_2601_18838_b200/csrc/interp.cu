@@ -395,6 +395,13 @@ __device__ __forceinline__ CellAxis cell_axis(const Geometry& g, int a, int i) {
 // accumulate phi in registers. The finished grid is contracted with the
 // cell's W2 slice, T1c[(i,j)][r] = sum_k phi[(i,j)][k] W2[r][c2 L + k], on
 // DMMA as well, into the warp's column partial of T1.
+#ifndef SPREAD_MINB
+#define SPREAD_MINB 3
+#endif
+#ifndef SPREAD_CH
+#define SPREAD_CH 16
+#endif
+
 template <int L>
 struct SpreadTile {
     static constexpr int L2 = L * L;
@@ -402,7 +409,7 @@ struct SpreadTile {
     static constexpr int MT2 = (L2 + 7) / 8;  // m-tiles of the contraction (rows (i,j))
     static constexpr int KS2 = (L + 3) / 4;   // k-steps of the contraction
     static constexpr int LDK = KS2 * 4;       // phi[(i,j)][k] row stride
-    static constexpr int CH = 16;             // particles staged per chunk
+    static constexpr int CH = SPREAD_CH;      // particles staged per chunk (16: lane pairs)
     static constexpr int LDP = CH + 4;        // staged row stride (conflict-free fragments)
     static constexpr int NW = 4;              // warps per CTA
     static constexpr int stage = (8 + NT * 8) * LDP;
@@ -414,9 +421,7 @@ __host__ __device__ constexpr int spread_warp_doubles(int R) {
     return SpreadTile<L>::stage + SpreadTile<L>::MT2 * 8 * ((R + 7) / 8) * 8;
 }
 
-#ifndef SPREAD_MINB
-#define SPREAD_MINB 3
-#endif
+
 // Staging rows that are identically zero (A rows >= L, B rows >= L^2); the
 // chunk loop never writes them, so they are cleared once per cell reuse.
 template <int L>
@@ -446,7 +451,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
     lagrange_consts(L, lc);
     for (int e = lane; e < MT2 * 8 * RP; e += 32) t1w[e] = 0.0;
     const CellAxis ax0 = cell_axis(g, 0, cr.c0), ax1 = cell_axis(g, 1, cr.c1);
-    const int p = lane & (CH - 1), half = lane >> 4;
+    const int p = lane & (CH - 1), half = CH == 32 ? 0 : lane >> 4;
     double qsum = 0.0;
     zero_padding<L>(As, Bs, lane);
     __syncthreads();
@@ -497,22 +502,32 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
                 lagrange_fast<L>(lc, ax2.lo, ax2.hi, ax2.mid, ax2.inv, pt.z, w2, a.bad);
             }
             __syncwarp();
-            // lane pair (p, p+16): A rows [4h, 4h+4) and B rows j in [JH h, JH h + JH)
+            if constexpr (CH == 32) {
+                // one particle per lane: its A row (q w0) and B row (w1 (x) w2)
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (i < L) {
-                    const double lo_w = w0[i], hi_w = (4 + i < L) ? w0[4 + i < L ? 4 + i : 0] : 0.0;
-                    As[(half * 4 + i) * LDP + p] = qv * (half ? hi_w : lo_w);  // rows >= L get 0
+                for (int i = 0; i < L; ++i) As[i * LDP + p] = qv * w0[i];
+#pragma unroll
+                for (int jj = 0; jj < L; ++jj)
+#pragma unroll
+                    for (int kk = 0; kk < L; ++kk) Bs[(jj * L + kk) * LDP + p] = w1[jj] * w2[kk];
+            } else {
+                // lane pair (p, p+16): A rows [4h, 4h+4) and B rows j in [JH h, JH h + JH)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (i < L) {
+                        const double lo_w = w0[i], hi_w = (4 + i < L) ? w0[4 + i < L ? 4 + i : 0] : 0.0;
+                        As[(half * 4 + i) * LDP + p] = qv * (half ? hi_w : lo_w);  // rows >= L get 0
+                    }
+                constexpr int JH = (L + 1) / 2;
+#pragma unroll
+                for (int jj = 0; jj < JH; ++jj) {
+                    const double a_lo = w1[jj];
+                    const double a_hi = (JH + jj < L) ? w1[JH + jj < L ? JH + jj : 0] : 0.0;
+                    const double wj = half ? a_hi : a_lo;
+                    const int row = (half * JH + jj) * L;
+#pragma unroll
+                    for (int kk = 0; kk < L; ++kk) Bs[(row + kk) * LDP + p] = wj * w2[kk];  // rows >= L^2 get 0
                 }
-            constexpr int JH = (L + 1) / 2;
-#pragma unroll
-            for (int jj = 0; jj < JH; ++jj) {
-                const double a_lo = w1[jj];
-                const double a_hi = (JH + jj < L) ? w1[JH + jj < L ? JH + jj : 0] : 0.0;
-                const double wj = half ? a_hi : a_lo;
-                const int row = (half * JH + jj) * L;
-#pragma unroll
-                for (int kk = 0; kk < L; ++kk) Bs[(row + kk) * LDP + p] = wj * w2[kk];  // rows >= L^2 get 0
             }
             __syncwarp();
             const int ks = (cnt + 3) >> 2;

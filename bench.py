@@ -405,7 +405,7 @@ def run_ours(a):
         line["cpu_baseline"] = cb
     if world == 1 and not slab and not a.no_extras:
         line["extras"] = extras(torch, dev, flush, a.steps)
-    print(json.dumps(line), flush=True)
+    emit(line)
     if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
@@ -471,10 +471,25 @@ def run_reference(a):
             "impl": "reference", "cpu_baseline": {**cb, "cpu": cpu_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_JSON_OUT = None
+
+
+def emit(line: dict):
+    """The one JSON line, on the real stdout (library banners such as NCCL's
+    version line are routed to stderr for the whole run)."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     a = args_()
     if a.impl == "reference":
         run_reference(a)

@@ -90,6 +90,8 @@ struct ColumnArgs {
     // monomial hot path: the W tables above are W_a Lambda (Lagrange basis ->
     // powers of the cell-local coordinate) and particles carry t^a, not w_k(t)
     int mono;
+    // per-axis cell tables (axis_lo, axis_hi, midpoint, 1/half-width), K_a each
+    const double4* cellax[3];
 };
 enum SpreadMode { SPREAD_PARTICLES = 0, SPREAD_FROM_CELLS = 1 };
 enum GatherMode { GATHER_FROM_B2 = 0, GATHER_FROM_CELLS = 1, PSI_ONLY = 2 };

@@ -377,6 +377,10 @@ __device__ __forceinline__ void powers(double lo, double hi, double mid, double 
 struct CellAxis {
     double lo, hi, mid, inv;
 };
+__device__ __forceinline__ CellAxis cell_axis_tab(const double4* tab, int i) {
+    const double4 v = tab[i];
+    return CellAxis{v.x, v.y, v.z, v.w};
+}
 __device__ __forceinline__ CellAxis cell_axis(const Geometry& g, int a, int i) {
     CellAxis c;
     c.lo = cell_lo(g, a, i);
@@ -400,6 +404,9 @@ __device__ __forceinline__ CellAxis cell_axis(const Geometry& g, int a, int i) {
 #endif
 #ifndef SPREAD_CH
 #define SPREAD_CH 16
+#endif
+#ifndef SPREAD_SKIP
+#define SPREAD_SKIP 0  // profiling ablations only: 1 DMMA loop, 2 staging, 4 prep, 8 contraction
 #endif
 
 template <int L>
@@ -450,7 +457,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
     __shared__ double red[128];
     lagrange_consts(L, lc);
     for (int e = lane; e < MT2 * 8 * RP; e += 32) t1w[e] = 0.0;
-    const CellAxis ax0 = cell_axis(g, 0, cr.c0), ax1 = cell_axis(g, 1, cr.c1);
+    const CellAxis ax0 = cell_axis_tab(a.cellax[0], cr.c0), ax1 = cell_axis_tab(a.cellax[1], cr.c1);
     const int p = lane & (CH - 1), half = CH == 32 ? 0 : lane >> 4;
     double qsum = 0.0;
     zero_padding<L>(As, Bs, lane);
@@ -479,7 +486,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
                 for (int node = lane; node < L3; node += 32) a.phi_cells[(int64_t)cell * L3 + node] = 0.0;
             continue;
         }
-        const CellAxis ax2 = cell_axis(g, 2, c2);
+        const CellAxis ax2 = cell_axis_tab(a.cellax[2], c2);
         double acc[NT][2];
 #pragma unroll
         for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
@@ -492,7 +499,10 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
             double w0[L], w1[L], w2[L];
             const double qv = p < cnt ? pt.w : 0.0;
             qsum += half == 0 ? qv : 0.0;
-            if (MONO) {
+            if (SPREAD_SKIP & 4) {
+#pragma unroll
+                for (int k = 0; k < L; ++k) w0[k] = w1[k] = w2[k] = pt.x + k;
+            } else if (MONO) {
                 powers<L>(ax0.lo, ax0.hi, ax0.mid, ax0.inv, pt.x, w0, a.bad);
                 powers<L>(ax1.lo, ax1.hi, ax1.mid, ax1.inv, pt.y, w1, a.bad);
                 powers<L>(ax2.lo, ax2.hi, ax2.mid, ax2.inv, pt.z, w2, a.bad);
@@ -502,7 +512,9 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
                 lagrange_fast<L>(lc, ax2.lo, ax2.hi, ax2.mid, ax2.inv, pt.z, w2, a.bad);
             }
             __syncwarp();
-            if constexpr (CH == 32) {
+            if (SPREAD_SKIP & 2) {
+                As[p] = qv * w0[0] * w1[1] * w2[2];
+            } else if constexpr (CH == 32) {
                 // one particle per lane: its A row (q w0) and B row (w1 (x) w2)
 #pragma unroll
                 for (int i = 0; i < L; ++i) As[i * LDP + p] = qv * w0[i];
@@ -530,7 +542,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
                 }
             }
             __syncwarp();
-            const int ks = (cnt + 3) >> 2;
+            const int ks = (SPREAD_SKIP & 1) ? 0 : (cnt + 3) >> 2;
             for (int kk = 0; kk < ks; ++kk) {
                 const int col = kk * 4 + (lane & 3);
                 const double af = As[(lane >> 2) * LDP + col];
@@ -555,7 +567,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
         if (a.phi_cells)
             for (int node = lane; node < L3; node += 32)
                 a.phi_cells[(int64_t)cell * L3 + node] = ph[(node / L) * LDK + node % L];
-        if (want_fwd) {
+        if (want_fwd && !(SPREAD_SKIP & 8)) {
             // T1c = ph[(i,j)][k] (MT2*8 x LDK) . W2s[k][r] (LDK x RP)
             double bf[KS2][4];
             const double* w2g = a.W2 + c2 * L;
@@ -609,16 +621,20 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
             tc[e] = s;
         }
         __syncthreads();
-        const double* w1 = a.W1 + cr.c1 * L;
+        double* w01 = u + L * R * R;  // [2][R][L] the column's W0 / W1 rows
+        for (int e = threadIdx.x; e < R * L; e += 128) {
+            w01[e] = a.W0[(int64_t)(e / L) * g.n[0] + cr.c0 * L + e % L];
+            w01[R * L + e] = a.W1[(int64_t)(e / L) * g.n[1] + cr.c1 * L + e % L];
+        }
+        __syncthreads();
         for (int e = threadIdx.x; e < L * R * R; e += 128) {
             const int i = e / (R * R), r1 = (e / R) % R, r2 = e % R;
             double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < L; ++j) s = fma(__ldg(w1 + (int64_t)r1 * g.n[1] + j), tc[(i * L + j) * R + r2], s);
+            for (int j = 0; j < L; ++j) s = fma(w01[R * L + r1 * L + j], tc[(i * L + j) * R + r2], s);
             u[e] = s;
         }
         __syncthreads();
-        const double* w0 = a.W0 + cr.c0 * L;
         // Fpart is entry-major, [R^3+1][nblocks], so k_core_sum reads it coalesced
         const int nblocks = a.S * g.K[0] * g.K[1];
         double* dst = a.Fpart + (int64_t)cr.seg * g.K[0] * g.K[1] + cr.col;
@@ -626,7 +642,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
             const int r0 = e / (R * R), rr = e % (R * R);
             double s = 0.0;
 #pragma unroll
-            for (int i = 0; i < L; ++i) s = fma(__ldg(w0 + (int64_t)r0 * g.n[0] + i), u[i * R * R + rr], s);
+            for (int i = 0; i < L; ++i) s = fma(w01[r0 * L + i], u[i * R * R + rr], s);
             dst[(int64_t)e * nblocks] = s;
         }
         __syncthreads();
@@ -708,7 +724,7 @@ __global__ void __launch_bounds__(GT, 512 / GT) k_bwd_gather_t(ColumnArgs a, int
             b2s[e] = a.B2[((int64_t)(cr.c0 * L + i) * g.n[1] + cr.c1 * L + j) * R + r];
         }
     }
-    const CellAxis ax0 = cell_axis(g, 0, cr.c0), ax1 = cell_axis(g, 1, cr.c1);
+    const CellAxis ax0 = cell_axis_tab(a.cellax[0], cr.c0), ax1 = cell_axis_tab(a.cellax[1], cr.c1);
     __syncthreads();
     double* w2s = psi + (size_t)cells_per_batch * L3 + (size_t)R * R * R + (size_t)L * R * R +
                   2 * (size_t)R * L;  // [R][cells_per_batch * L] W2 slice of the batch
@@ -789,7 +805,7 @@ __global__ void __launch_bounds__(GT, 512 / GT) k_bwd_gather_t(ColumnArgs a, int
                 }
                 const int c2 = axis_cell(p.z, g.center[2], g.radius, g.K[2], g.inv_diam);
                 const double* ps = psi + (c2 - cb0) * L3;
-                const CellAxis ax2 = cell_axis(g, 2, c2);
+                const CellAxis ax2 = cell_axis_tab(a.cellax[2], c2);
                 double z = 0.0;
                 if (MONO) {
                     // ps = monomial coefficients C[a][b][c] of this cell's potential:
@@ -862,7 +878,7 @@ template <int L, bool MONO>
 void launch_spread_mma_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
     const int R = a.g.R;
     const size_t smem = sizeof(double) * (SpreadTile<L>::NW * spread_warp_doubles<L>(R) +
-                                          (size_t)L * L * R + (size_t)L * R * R);
+                                          (size_t)L * L * R + (size_t)L * R * R + 2 * (size_t)R * L);
     static int attr_done = 0;
     if (!attr_done) {
         KB_CUDA(cudaFuncSetAttribute(k_spread_mma<L, MONO>,

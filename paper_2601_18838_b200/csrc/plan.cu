@@ -42,6 +42,7 @@ struct kpme_gpu_plan_s {
     double* W[3] = {nullptr, nullptr, nullptr};
     double* WL[3] = {nullptr, nullptr, nullptr};  // W_a Lambda (monomial hot path)
     double* lam = nullptr;
+    double4* cellax = nullptr;  // [K0 + K1 + K2] (lo, hi, mid, 1/half)
     double* D = nullptr;
     double* G = nullptr;
     // collapsed-core work
@@ -169,6 +170,9 @@ kb::ColumnArgs column_args(kpme_gpu_plan p) {
     a.W0 = p->W[0];
     a.W1 = p->W[1];
     a.Gc = p->G;
+    a.cellax[0] = p->cellax;
+    a.cellax[1] = p->cellax + p->g.K[0];
+    a.cellax[2] = p->cellax + p->g.K[0] + p->g.K[1];
     a.correction = p->correction;
     return a;
 }
@@ -398,6 +402,20 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, in
             p->sp = p->alloc<double4>(p->cap);
             KB_CUDA(cudaMallocHost(&p->flags_h, 2 * sizeof(unsigned long long)));
             KB_CUDA(cudaMemsetAsync(p->colq, 0, sizeof(double) * p->S * ncol, p->stream));
+            {
+                // CellGrid::axis_lo / axis_hi (geometry.hpp:90-98) per axis and cell,
+                // plus the midpoint and inverse half-width used by the weights
+                std::vector<double4> tab;
+                for (int a = 0; a < 3; ++a)
+                    for (int i = 0; i < g.K[a]; ++i) {
+                        const double lo = g.center[a] - g.radius + 2.0 * g.radius * i / g.K[a];
+                        const double hi = g.center[a] - g.radius + 2.0 * g.radius * (i + 1) / g.K[a];
+                        tab.push_back(make_double4(lo, hi, 0.5 * (hi + lo), 1.0 / (0.5 * (hi - lo))));
+                    }
+                p->cellax = p->alloc<double4>(tab.size());
+                KB_CUDA(cudaMemcpy(p->cellax, tab.data(), sizeof(double4) * tab.size(),
+                                   cudaMemcpyHostToDevice));
+            }
             kb::launch_factor_tables(g, p->nterms, p->tw, p->prof, p->W[0], p->W[1], p->W[2], p->D,
                                      p->G, p->stream);
             if (L <= 8) {

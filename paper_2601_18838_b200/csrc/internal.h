@@ -52,6 +52,10 @@ struct SortBuffers {
     int32_t* rank;        // [n] provisional slot within the cell
     int32_t* perm;        // [n]
     double4* rec;         // [n] particle records at their provisional slots
+    // two-level counting sort (sort2.cu)
+    int32_t* hist;        // [ncol * ntiles] per-tile column histogram, then its scan
+    int32_t* ctot;        // [ncol] column totals
+    int2* kz2;            // [n] column-ordered (particle index, c2)
     int32_t* big;         // [ncell] cells too large for the warp sorter
     int32_t* nbig;        // [1]
     unsigned long long* bad;  // [2]: lowest out-of-box index, out-of-cell flag
@@ -59,6 +63,10 @@ struct SortBuffers {
 // Also writes the sorted particles sp (x, y, z, q) when q and sp are given.
 void launch_sort(const Geometry& g, int64_t n, const double* xyz, const SortBuffers& b,
                  cudaStream_t s, int* launches, const double* q = nullptr, double4* sp = nullptr);
+bool sort2_supported(const Geometry& g);
+size_t sort2_hist_entries(const Geometry& g, int64_t cap);
+void launch_sort2(const Geometry& g, int64_t n, const double* xyz, const SortBuffers& b,
+                  cudaStream_t s, int* launches, const double* q = nullptr, double4* sp = nullptr);
 void launch_permute(int64_t n, const double* xyz, const double* q, const int32_t* perm,
                     double4* sp, cudaStream_t s);
 

@@ -35,6 +35,7 @@ struct kpme_gpu_plan_s {
     int form = KPME_GPU_FORM_COLLAPSED;
     int launches = 0;
     int64_t last_n = 0;
+    bool use_sort2 = false;
 
     // factor tables
     double* tw = nullptr;
@@ -178,8 +179,11 @@ kb::ColumnArgs column_args(kpme_gpu_plan p) {
 }
 
 void sort_and_permute(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q) {
-    // the segment sort also writes the sorted particles when q is given
-    kb::launch_sort(p->g, n, xyz, p->sb, p->stream, &p->launches, q, q ? p->sp : nullptr);
+    // the sort also writes the cell-ordered particle records when q is given
+    if (p->use_sort2)
+        kb::launch_sort2(p->g, n, xyz, p->sb, p->stream, &p->launches, q, q ? p->sp : nullptr);
+    else
+        kb::launch_sort(p->g, n, xyz, p->sb, p->stream, &p->launches, q, q ? p->sp : nullptr);
 }
 
 // Hot path for L <= 8: factor rows in the monomial basis of each cell.
@@ -395,6 +399,13 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, in
             p->sb.key = p->alloc<int32_t>(p->cap);
             p->sb.rank = p->alloc<int32_t>(p->cap);
             p->sb.rec = p->alloc<double4>(p->cap);
+            p->use_sort2 = kb::sort2_supported(g);
+            if (p->use_sort2) {
+                const size_t E = kb::sort2_hist_entries(g, p->cap);
+                p->sb.hist = p->alloc<int32_t>(E);
+                p->sb.ctot = p->alloc<int32_t>((size_t)g.K[0] * g.K[1]);
+                p->sb.kz2 = p->alloc<int2>(p->cap);
+            }
             p->sb.perm = p->alloc<int32_t>(p->cap);
             p->sb.big = p->alloc<int32_t>(g.ncell);
             p->sb.nbig = p->alloc<int32_t>(1);
@@ -675,7 +686,7 @@ extern "C" int kpme_gpu_gather(kpme_gpu_plan p, int64_t n, const double* xyz,
         KB_CUDA(cudaSetDevice(p->device));
         reset_flags(p);
         // the permute needs charges; gather ignores them, pass positions twice
-        kb::launch_sort(p->g, n, xyz, p->sb, p->stream, &p->launches);
+        sort_and_permute(p, n, xyz, nullptr);
         kb::launch_permute(n, xyz, xyz, p->sb.perm, p->sp, p->stream);
         kb::ColumnArgs a = column_args(p);
         a.psi_cells = const_cast<double*>(psi_cells);

@@ -1,0 +1,494 @@
+// sort2.cu -- two-level stable counting sort into cell order (the default
+// cell sort; sort.cu's atomic-slot sort is the fallback for very large grids).
+//
+// The reference's order (assign_particles, geometry.hpp:131-154) is: cells in
+// flatten order (c0, c1, c2), particles ascending inside each cell. Here:
+//   k_tile_hist   cell key (exact arithmetic, shared with sort.cu) and a
+//                 per-tile histogram over columns (c0, c1)
+//   k_col_scan    per column: exclusive scan over tiles, column totals
+//   k_col_scatter stable scatter by column: inside a tile, ranks come from
+//                 warp ballots in particle order plus per-warp offsets, so
+//                 every column segment keeps ascending particle order; writes
+//                 the packed (index, c2) pair and the particle record
+//   k_z_sort      one CTA per column: stable counting sort by c2 in chunks
+//                 staged in shared memory, so perm and the cell-ordered
+//                 records leave in coalesced runs; writes cell_start
+// No global atomics; the result is deterministic and equals the reference.
+//
+// Scattered global stores cost one L2 request per lane (measured:
+// scripts/probes/scatter_probe.cu), so the design keeps them to one packed
+// 8-byte pair plus one 32-byte record per particle (column scatter) and
+// stages the per-column pass in shared memory.
+#include <algorithm>
+#include <climits>
+#include <type_traits>
+
+#include "internal.h"
+
+namespace kb {
+namespace {
+
+#ifndef SORT2_ROUNDS
+#define SORT2_ROUNDS 8
+#endif
+#ifndef SORT2_ZROUNDS
+#define SORT2_ZROUNDS 4
+#endif
+constexpr int kTileWarps = 8;
+constexpr int kRounds = SORT2_ROUNDS;             // 32-particle rounds per warp
+constexpr int kTile = kTileWarps * kRounds * 32;  // particles per tile (2048)
+constexpr int kHistThreads = kTile / 4;           // 4 particles per thread
+constexpr int kGroup = 4;                         // rounds whose loads are issued together
+constexpr int kZWarps = 8;                        // warps per column CTA in k_z_sort
+constexpr int kZRounds = SORT2_ZROUNDS;
+constexpr int kZChunk = kZWarps * kZRounds * 32;  // column elements staged per chunk
+static_assert(kRounds % kGroup == 0, "rounds come in load groups");
+
+// Markstein-division axis cell, identical to sort.cu's axis_cell:
+__device__ __forceinline__ int axis_cell2(double p, double c, double r, int K, double b,
+                                          double y) {
+    const double a = __dmul_rn(__dsub_rn(p, __dsub_rn(c, r)), (double)K);
+    const double q0 = __dmul_rn(a, y);
+    const double t = __fma_rn(__fma_rn(-q0, b, a), y, q0);
+    int idx = (int)floor(t);
+    if (t == (double)idx && idx > 0) --idx;
+    if (idx < 0) idx = 0;
+    if (idx > K - 1) idx = K - 1;
+    return idx;
+}
+
+// Lanes of the warp holding the same non-negative key (inactive lanes pass a
+// negative key and are never anyone's peer): one ballot per key bit, NB known
+// at compile time (keys are < 2^NB). MATCH.ANY measured slower on B200.
+template <int NB>
+__device__ __forceinline__ unsigned warp_peers(int v) {
+    unsigned m = __ballot_sync(0xffffffffu, v >= 0);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const bool bit = (v >> b) & 1;
+        const unsigned bb = __ballot_sync(0xffffffffu, bit);
+        m &= bit ? bb : ~bb;
+    }
+    return m;
+}
+
+__host__ __device__ inline int bits_for(int count) {  // bits to hold 0..count-1
+    int b = 0;
+    while ((1 << b) < count) ++b;
+    return b;
+}
+
+// Cell keys + box check + per-tile column histogram hist[col * ntiles + tile].
+__global__ void __launch_bounds__(kHistThreads) k_tile_hist(Geometry g, int64_t n,
+                                                   const double* __restrict__ xyz,
+                                                   int32_t* __restrict__ key,
+                                                   int32_t* __restrict__ hist, int ntiles,
+                                                   unsigned long long* bad) {
+    extern __shared__ int32_t h[];  // [ncol]
+    const int ncol = g.K[0] * g.K[1];
+    for (int c = threadIdx.x; c < ncol; c += blockDim.x) h[c] = 0;
+    __syncthreads();
+    const int64_t t0 = (int64_t)blockIdx.x * kTile;
+    const double b = __dmul_rn(2.0, g.radius), y = g.inv_diam;
+    constexpr int kPer = kTile / kHistThreads;
+    double p[kPer][3];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {  // issue every load of the tile first
+        const int64_t i = t0 + u * kHistThreads + threadIdx.x;
+        if (i < n) {
+            p[u][0] = __ldg(xyz + 3 * i);
+            p[u][1] = __ldg(xyz + 3 * i + 1);
+            p[u][2] = __ldg(xyz + 3 * i + 2);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const int64_t i = t0 + u * kHistThreads + threadIdx.x;
+        if (i >= n) break;
+        const double p0 = p[u][0], p1 = p[u][1], p2 = p[u][2];
+        if (fabs(p0 - g.center[0]) > g.radius || fabs(p1 - g.center[1]) > g.radius ||
+            fabs(p2 - g.center[2]) > g.radius)
+            atomicMin(&bad[0], (unsigned long long)i);  // Box3::contains (geometry.hpp:36-40)
+        const int c0 = axis_cell2(p0, g.center[0], g.radius, g.K[0], b, y);
+        const int c1 = axis_cell2(p1, g.center[1], g.radius, g.K[1], b, y);
+        const int c2 = axis_cell2(p2, g.center[2], g.radius, g.K[2], b, y);
+        if (c2 < g.z_lo || c2 >= g.z_hi) atomicOr(&bad[1], 2ull);
+        key[i] = (c0 * g.K[1] + c1) * g.K[2] + c2;
+        atomicAdd(&h[c0 * g.K[1] + c1], 1);  // shared-memory counter, order irrelevant
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < ncol; c += blockDim.x) hist[(int64_t)c * ntiles + blockIdx.x] = h[c];
+}
+
+// Warp per column: exclusive scan of hist[col][0..ntiles) in place, column
+// total to ctot[col]. Loads are issued kScanBatch x 32 at a time.
+constexpr int kScanBatch = 8;
+__global__ void __launch_bounds__(256) k_col_scan(int ncol, int ntiles, int32_t* __restrict__ hist,
+                                                  int32_t* __restrict__ ctot) {
+    const int col = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (col >= ncol) return;
+    int32_t* row = hist + (int64_t)col * ntiles;
+    int carry = 0;
+    for (int b0 = 0; b0 < ntiles; b0 += 32 * kScanBatch) {
+        int v[kScanBatch];
+#pragma unroll
+        for (int u = 0; u < kScanBatch; ++u) {
+            const int t = b0 + u * 32 + lane;
+            v[u] = t < ntiles ? row[t] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kScanBatch; ++u) {
+            int x = v[u];
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            const int t = b0 + u * 32 + lane;
+            if (t < ntiles) row[t] = carry + x - v[u];
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+    }
+    if (lane == 0) ctot[col] = carry;
+}
+
+// Exclusive scan of ctot[0..ncol) into shared memory out[0..ncol], out[ncol] =
+// total; whole CTA (blockDim a multiple of 32, <= 1024); ends synchronised.
+__device__ void block_col_bases(const int32_t* __restrict__ ctot, int ncol, int32_t* out,
+                                int32_t* wsum /* [32] */) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nt = blockDim.x;
+    const int per = (ncol + nt - 1) / nt;
+    const int lo = min(ncol, tid * per), hi = min(ncol, lo + per);
+    int s = 0;
+    for (int c = lo; c < hi; ++c) s += ctot[c];
+    int x = s;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int t = lane < (nt >> 5) ? wsum[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        wsum[lane] = t;
+    }
+    __syncthreads();
+    int run = (w > 0 ? wsum[w - 1] : 0) + x - s;
+    for (int c = lo; c < hi; ++c) {
+        out[c] = run;
+        run += ctot[c];
+    }
+    if (tid == nt - 1) out[ncol] = run;
+    __syncthreads();
+}
+
+// Stable scatter by column. Warp w of tile t owns particles
+// [t*kTile + w*kRounds*32, +kRounds*32), processed 32 at a time in index order.
+// The warp's keys are loaded into registers once and the record loads of
+// kGroup rounds are issued together.
+template <int CB>
+__global__ void __launch_bounds__(kTileWarps * 32) k_col_scatter(Geometry g, int64_t n, int ntiles,
+                                                                 const int32_t* __restrict__ key,
+                                                                 const int32_t* __restrict__ cscan,
+                                                                 const int32_t* __restrict__ ctot,
+                                                                 const double* __restrict__ xyz,
+                                                                 const double* __restrict__ q,
+                                                                 int2* __restrict__ kz2,
+                                                                 double4* __restrict__ rec2) {
+    extern __shared__ int32_t wc[];  // [kTileWarps][ncol] per-warp column counters, then bases
+    __shared__ int32_t wsum[32];
+    const int ncol = g.K[0] * g.K[1], K2 = g.K[2];
+    int32_t* cbase = wc + kTileWarps * ncol;  // [ncol + 1]
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int e = threadIdx.x; e < kTileWarps * ncol; e += blockDim.x) wc[e] = 0;
+    const int64_t wbase = (int64_t)blockIdx.x * kTile + w * (kRounds * 32);
+    int kreg[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t i = wbase + r * 32 + lane;
+        kreg[r] = i < n ? __ldg(key + i) : -1;
+    }
+    block_col_bases(ctot, ncol, cbase, wsum);  // also orders the zeroing above
+    // 1: per-warp column counts
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const bool act = kreg[r] >= 0;
+        const int col = act ? kreg[r] / K2 : -1 - lane;
+        const unsigned peers = warp_peers<CB>(col);
+        if (act && lane == __ffs(peers) - 1) wc[w * ncol + col] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // 2: exclusive prefix over warps, plus this tile's global column offset
+    for (int c = threadIdx.x; c < ncol; c += blockDim.x) {
+        int run = cbase[c] + cscan[(int64_t)c * ntiles + blockIdx.x];
+        for (int k = 0; k < kTileWarps; ++k) {
+            const int t = wc[k * ncol + c];
+            wc[k * ncol + c] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+    // 3: placement in index order
+#pragma unroll
+    for (int r0 = 0; r0 < kRounds; r0 += kGroup) {
+        double4 v[kGroup];
+        if (rec2) {
+#pragma unroll
+            for (int u = 0; u < kGroup; ++u) {
+                const int64_t i = wbase + (r0 + u) * 32 + lane;
+                if (kreg[r0 + u] >= 0)
+                    v[u] = make_double4(__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1),
+                                        __ldg(xyz + 3 * i + 2), __ldg(q + i));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kGroup; ++u) {
+            const int r = r0 + u;
+            const int k = kreg[r];
+            const bool act = k >= 0;
+            const int col = act ? k / K2 : -1 - lane;
+            const unsigned peers = warp_peers<CB>(col);
+            if (act) {
+                const int pos = wc[w * ncol + col] + __popc(peers & ((1u << lane) - 1));
+                kz2[pos] = make_int2((int)(wbase + r * 32 + lane), k - col * K2);
+                if (rec2) rec2[pos] = v[u];
+            }
+            __syncwarp();
+            if (act && lane == __ffs(peers) - 1) wc[w * ncol + col] += __popc(peers);
+            __syncwarp();
+        }
+    }
+}
+
+// Shared-memory layout of k_z_sort (bytes), for K2 cells per column.
+struct ZLayout {
+    size_t rec, idx, z, cnt, zrun, lstart, total;
+    __host__ __device__ ZLayout(int K2, bool with_rec) {
+        rec = 0;
+        idx = with_rec ? sizeof(double4) * kZChunk : 0;
+        z = idx + sizeof(int32_t) * kZChunk;
+        cnt = z + sizeof(uint16_t) * kZChunk;
+        cnt = (cnt + 15) & ~size_t(15);
+        zrun = cnt + sizeof(int32_t) * kZWarps * K2;
+        lstart = zrun + sizeof(int32_t) * K2;
+        total = lstart + sizeof(int32_t) * (K2 + 1);
+    }
+};
+
+// One CTA per column: stable counting sort of the column segment by c2. The
+// segment is taken kZChunk elements at a time (warp w owns a contiguous
+// kZRounds x 32 slice of the chunk); each chunk is ranked into shared memory in
+// (c2, particle) order and written out as contiguous per-cell runs.
+template <int ZB>
+__global__ void __launch_bounds__(kZWarps * 32, 3) k_z_sort(Geometry g,
+                                                         const int32_t* __restrict__ ctot,
+                                                         int64_t n,
+                                                         const int2* __restrict__ kz2,
+                                                         const double4* __restrict__ rec2,
+                                                         int32_t* __restrict__ perm,
+                                                         int32_t* __restrict__ start,
+                                                         double4* __restrict__ sp) {
+    extern __shared__ __align__(16) unsigned char zsm[];
+    __shared__ int32_t wsum[32];
+    __shared__ int32_t red[kZWarps];
+    const int K2 = g.K[2], ncol = g.K[0] * g.K[1];
+    const ZLayout L(K2, sp != nullptr);
+    double4* s_rec = reinterpret_cast<double4*>(zsm + L.rec);
+    int32_t* s_idx = reinterpret_cast<int32_t*>(zsm + L.idx);
+    uint16_t* s_z = reinterpret_cast<uint16_t*>(zsm + L.z);
+    int32_t* cnt = reinterpret_cast<int32_t*>(zsm + L.cnt);  // [K2][kZWarps]
+    int32_t* zrun = reinterpret_cast<int32_t*>(zsm + L.zrun);
+    int32_t* lstart = reinterpret_cast<int32_t*>(zsm + L.lstart);
+    const int col = blockIdx.x, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    (void)wsum;
+    // column start = sum of the totals of the columns before it
+    int s = 0;
+    for (int c = tid; c < col; c += blockDim.x) s += ctot[c];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[w] = s;
+    for (int e = tid; e < K2; e += blockDim.x) zrun[e] = 0;
+    __syncthreads();
+    int cs = 0;
+    for (int k = 0; k < kZWarps; ++k) cs += red[k];
+    const int m = ctot[col];
+    const int2* seg = kz2 + cs;
+    // column histogram over c2 (order-free)
+    for (int j0 = 0; j0 < m; j0 += 4 * kZWarps * 32) {
+        int zz[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u * kZWarps * 32 + tid;
+            zz[u] = j < m ? __ldg(&seg[j].y) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (zz[u] >= 0) atomicAdd(&zrun[zz[u]], 1);
+    }
+    __syncthreads();
+    if (w == 0) {  // cell starts; zrun becomes each cell's running output position
+        int carry = cs;
+        for (int base = 0; base < K2; base += 32) {
+            const int z = base + lane;
+            const int own = z < K2 ? zrun[z] : 0;
+            int x = own;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (z < K2) {
+                zrun[z] = carry + x - own;
+                start[(int64_t)col * K2 + z] = carry + x - own;
+            }
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (col == ncol - 1 && lane == 0) start[(int64_t)ncol * K2] = (int)n;
+    }
+    for (int c0 = 0; c0 < m; c0 += kZChunk) {
+        const int cm = min(kZChunk, m - c0);
+        for (int e = tid; e < kZWarps * K2; e += blockDim.x) cnt[e] = 0;
+        int zr[kZRounds], ir[kZRounds];
+        double4 v[kZRounds];
+#pragma unroll
+        for (int u = 0; u < kZRounds; ++u) {
+            const int jl = w * (kZRounds * 32) + u * 32 + lane;
+            const bool act = jl < cm;
+            int2 kz = act ? seg[c0 + jl] : make_int2(0, -1 - lane);
+            zr[u] = kz.y;
+            ir[u] = kz.x;
+            if (sp && act) v[u] = rec2[cs + c0 + jl];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kZRounds; ++u) {
+            const unsigned peers = warp_peers<ZB>(zr[u]);
+            if (zr[u] >= 0 && lane == __ffs(peers) - 1) cnt[zr[u] * kZWarps + w] += __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        if (w == 0) {  // exclusive scan in (c2, warp) order; chunk-local cell starts
+            int carry = 0;
+            const int E = K2 * kZWarps;
+            for (int base = 0; base < E; base += 32) {
+                const int e = base + lane;
+                const int own = e < E ? cnt[e] : 0;
+                int x = own;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (e < E) {
+                    cnt[e] = carry + x - own;
+                    if (e % kZWarps == 0) lstart[e / kZWarps] = carry + x - own;
+                }
+                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
+            if (lane == 0) lstart[K2] = carry;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kZRounds; ++u) {
+            const bool act = zr[u] >= 0;
+            const unsigned peers = warp_peers<ZB>(zr[u]);
+            if (act) {
+                const int lp = cnt[zr[u] * kZWarps + w] + __popc(peers & ((1u << lane) - 1));
+                s_idx[lp] = ir[u];
+                s_z[lp] = (uint16_t)zr[u];
+                if (sp) s_rec[lp] = v[u];
+            }
+            __syncwarp();
+            if (act && lane == __ffs(peers) - 1) cnt[zr[u] * kZWarps + w] += __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        for (int k = tid; k < cm; k += blockDim.x) {  // contiguous per-cell runs
+            const int z = s_z[k];
+            const int gp = zrun[z] + (k - lstart[z]);
+            perm[gp] = s_idx[k];
+            if (sp) sp[gp] = s_rec[k];
+        }
+        __syncthreads();
+        for (int z = tid; z < K2; z += blockDim.x) zrun[z] += lstart[z + 1] - lstart[z];
+    }
+}
+
+// Instantiation for an even key width in [2, 16].
+template <class F>
+auto pick_bits(int b, F f) {
+    switch (b) {
+        case 2: return f(std::integral_constant<int, 2>{});
+        case 4: return f(std::integral_constant<int, 4>{});
+        case 6: return f(std::integral_constant<int, 6>{});
+        case 8: return f(std::integral_constant<int, 8>{});
+        case 10: return f(std::integral_constant<int, 10>{});
+        case 12: return f(std::integral_constant<int, 12>{});
+        case 14: return f(std::integral_constant<int, 14>{});
+        default: return f(std::integral_constant<int, 16>{});
+    }
+}
+
+}  // namespace
+
+bool sort2_supported(const Geometry& g) {
+    const int ncol = g.K[0] * g.K[1];
+    return (size_t)(kTileWarps * ncol + ncol + 1) * sizeof(int32_t) <= 160 * 1024 &&
+           ZLayout(g.K[2], true).total <= 160 * 1024 && ncol <= 65536 && g.K[2] <= 65536;
+}
+
+size_t sort2_hist_entries(const Geometry& g, int64_t cap) {
+    const int64_t ntiles = (cap + kTile - 1) / kTile;
+    return (size_t)g.K[0] * g.K[1] * (size_t)std::max<int64_t>(1, ntiles);
+}
+
+void launch_sort2(const Geometry& g, int64_t n, const double* xyz, const SortBuffers& b,
+                  cudaStream_t s, int* launches, const double* q, double4* sp) {
+    if (!q) sp = nullptr;
+    // key widths rounded up to an even bit count (extra ballots see zero bits)
+    const int ncol = g.K[0] * g.K[1];
+    const int cb = (bits_for(ncol) + 1) & ~1, zb = (bits_for(g.K[2]) + 1) & ~1;
+    auto col_kernel = pick_bits(cb, [](auto B) { return &k_col_scatter<decltype(B)::value>; });
+    auto z_kernel = pick_bits(zb, [](auto B) { return &k_z_sort<decltype(B)::value>; });
+    static bool attr = false;
+    if (!attr) {
+        for (int b = 2; b <= 16; b += 2) {
+            KB_CUDA(cudaFuncSetAttribute(pick_bits(b, [](auto B) { return &k_col_scatter<decltype(B)::value>; }),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+            KB_CUDA(cudaFuncSetAttribute(pick_bits(b, [](auto B) { return &k_z_sort<decltype(B)::value>; }),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        }
+        KB_CUDA(cudaFuncSetAttribute(k_tile_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     160 * 1024));
+        attr = true;
+    }
+    const int ntiles = (int)std::max<int64_t>(1, (n + kTile - 1) / kTile);
+    const int64_t E = (int64_t)ncol * ntiles;
+    int l = 0;
+    if (n > 0) {
+        k_tile_hist<<<ntiles, kHistThreads, ncol * sizeof(int32_t), s>>>(g, n, xyz, b.key, b.hist,
+                                                                          ntiles, b.bad);
+        ++l;
+    } else {
+        KB_CUDA(cudaMemsetAsync(b.hist, 0, sizeof(int32_t) * E, s));
+    }
+    KB_CHECK_LAUNCH();
+    k_col_scan<<<(ncol + 7) / 8, 256, 0, s>>>(ncol, ntiles, b.hist, b.ctot);
+    KB_CHECK_LAUNCH();
+    ++l;
+    if (n > 0) {
+        col_kernel<<<ntiles, kTileWarps * 32, (kTileWarps * ncol + ncol + 1) * sizeof(int32_t),
+                        s>>>(g, n, ntiles, b.key, b.hist, b.ctot, xyz, q, b.kz2,
+                             sp ? b.rec : nullptr);
+        KB_CHECK_LAUNCH();
+        ++l;
+    }
+    z_kernel<<<ncol, kZWarps * 32, ZLayout(g.K[2], sp != nullptr).total, s>>>(
+        g, b.ctot, n, b.kz2, b.rec, b.perm, b.start, sp);
+    KB_CHECK_LAUNCH();
+    ++l;
+    if (launches) *launches += l;
+}
+
+}  // namespace kb

@@ -12,7 +12,7 @@ for flags in "$@"; do
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/var_$tag.csv \
       python scripts/profile_step.py cfg3 3 > /dev/null 2>&1
   echo "== $flags"
-  python scripts/launches.py gpurun_out/var_$tag.csv | grep -E "spread|gather|keys|place|segsort"
+  python scripts/launches.py gpurun_out/var_$tag.csv | grep -E "${SWEEP_GREP:-spread|gather|keys|place|segsort}"
 done
 make -C paper_2601_18838_b200/csrc clean > /dev/null
 make -C paper_2601_18838_b200/csrc -j8 > /dev/null 2>&1

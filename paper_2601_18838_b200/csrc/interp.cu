@@ -491,11 +491,11 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
 #pragma unroll
         for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
         // lanes past the chunk end clamp to a valid particle and carry q = 0
-        double4 nxt = a.sp[s0 + min(p, s1 - s0 - 1)];
+        double4 nxt = ld_rec(a.sp + s0 + min(p, s1 - s0 - 1));
         for (int base = s0; base < s1; base += CH) {
             const int cnt = min(CH, s1 - base);
             const double4 pt = nxt;  // software prefetch of the next chunk
-            if (base + CH < s1) nxt = a.sp[base + CH + min(p, s1 - base - CH - 1)];
+            if (base + CH < s1) nxt = ld_rec(a.sp + base + CH + min(p, s1 - base - CH - 1));
             double w0[L], w1[L], w2[L];
             const double qv = p < cnt ? pt.w : 0.0;
             qsum += half == 0 ? qv : 0.0;
@@ -794,13 +794,13 @@ __global__ void __launch_bounds__(GT, 512 / GT) k_bwd_gather_t(ColumnArgs a, int
         __syncthreads();
         if (MODE != PSI_ONLY) {
             const int s0 = a.start[cell0], s1 = a.start[cell0 + (cb1 - cb0)];
-            double4 pn = s0 + tid < s1 ? a.sp[s0 + tid] : make_double4(0.0, 0.0, 0.0, 0.0);
+            double4 pn = s0 + tid < s1 ? ld_rec(a.sp + s0 + tid) : make_double4(0.0, 0.0, 0.0, 0.0);
             int dn = s0 + tid < s1 ? a.perm[s0 + tid] : 0;
             for (int s = s0 + tid; s < s1; s += GT) {
                 const double4 p = pn;  // software prefetch of the next particle
                 const int dst = dn;
                 if (s + GT < s1) {
-                    pn = a.sp[s + GT];
+                    pn = ld_rec(a.sp + s + GT);
                     dn = a.perm[s + GT];
                 }
                 const int c2 = axis_cell(p.z, g.center[2], g.radius, g.K[2], g.inv_diam);

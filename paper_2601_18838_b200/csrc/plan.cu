@@ -404,7 +404,7 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, in
                 const size_t E = kb::sort2_hist_entries(g, p->cap);
                 p->sb.hist = p->alloc<int32_t>(E);
                 p->sb.ctot = p->alloc<int32_t>((size_t)g.K[0] * g.K[1]);
-                p->sb.kz2 = p->alloc<int2>(p->cap);
+                p->sb.kz2 = p->alloc<int2>(p->cap + 2);  // +2: 16-byte aligned bulk reads
             }
             p->sb.perm = p->alloc<int32_t>(p->cap);
             p->sb.big = p->alloc<int32_t>(g.ncell);

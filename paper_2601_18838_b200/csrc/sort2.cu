@@ -60,13 +60,24 @@ __device__ __forceinline__ int axis_cell2(double p, double c, double r, int K, d
 // Lanes of the warp holding the same non-negative key (inactive lanes pass a
 // negative key and are never anyone's peer): one ballot per key bit, NB known
 // at compile time (keys are < 2^NB). MATCH.ANY measured slower on B200.
+// The votes are volatile asm so the compiler keeps them in program order:
+// hoisting every round's ballots at once costs more registers than it saves.
+__device__ __forceinline__ unsigned vote_ballot(bool p) {
+    unsigned r;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tvote.sync.ballot.b32 %0, p, 0xffffffff;\n\t}"
+        : "=r"(r)
+        : "r"((unsigned)p));
+    return r;
+}
+
 template <int NB>
 __device__ __forceinline__ unsigned warp_peers(int v) {
-    unsigned m = __ballot_sync(0xffffffffu, v >= 0);
+    unsigned m = vote_ballot(v >= 0);
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
         const bool bit = (v >> b) & 1;
-        const unsigned bb = __ballot_sync(0xffffffffu, bit);
+        const unsigned bb = vote_ballot(bit);
         m &= bit ? bb : ~bb;
     }
     return m;
@@ -113,7 +124,7 @@ __global__ void __launch_bounds__(kHistThreads) k_tile_hist(Geometry g, int64_t 
         const int c1 = axis_cell2(p1, g.center[1], g.radius, g.K[1], b, y);
         const int c2 = axis_cell2(p2, g.center[2], g.radius, g.K[2], b, y);
         if (c2 < g.z_lo || c2 >= g.z_hi) atomicOr(&bad[1], 2ull);
-        key[i] = (c0 * g.K[1] + c1) * g.K[2] + c2;
+        key[i] = ((c0 * g.K[1] + c1) << 16) | c2;  // (column, c2) packed
         atomicAdd(&h[c0 * g.K[1] + c1], 1);  // shared-memory counter, order irrelevant
     }
     __syncthreads();
@@ -190,7 +201,7 @@ __device__ void block_col_bases(const int32_t* __restrict__ ctot, int ncol, int3
 // The warp's keys are loaded into registers once and the record loads of
 // kGroup rounds are issued together.
 template <int CB>
-__global__ void __launch_bounds__(kTileWarps * 32) k_col_scatter(Geometry g, int64_t n, int ntiles,
+__global__ void __launch_bounds__(kTileWarps * 32, 4) k_col_scatter(Geometry g, int64_t n, int ntiles,
                                                                  const int32_t* __restrict__ key,
                                                                  const int32_t* __restrict__ cscan,
                                                                  const int32_t* __restrict__ ctot,
@@ -200,7 +211,8 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_col_scatter(Geometry g, int
                                                                  double4* __restrict__ rec2) {
     extern __shared__ int32_t wc[];  // [kTileWarps][ncol] per-warp column counters, then bases
     __shared__ int32_t wsum[32];
-    const int ncol = g.K[0] * g.K[1], K2 = g.K[2];
+    __shared__ unsigned pm[kTileWarps][kRounds][32];  // phase-1 peer masks, reused in phase 3
+    const int ncol = g.K[0] * g.K[1];
     int32_t* cbase = wc + kTileWarps * ncol;  // [ncol + 1]
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int e = threadIdx.x; e < kTileWarps * ncol; e += blockDim.x) wc[e] = 0;
@@ -216,8 +228,9 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_col_scatter(Geometry g, int
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
         const bool act = kreg[r] >= 0;
-        const int col = act ? kreg[r] / K2 : -1 - lane;
+        const int col = act ? kreg[r] >> 16 : -1 - lane;
         const unsigned peers = warp_peers<CB>(col);
+        pm[w][r][lane] = peers;
         if (act && lane == __ffs(peers) - 1) wc[w * ncol + col] += __popc(peers);
         __syncwarp();
     }
@@ -232,34 +245,38 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_col_scatter(Geometry g, int
         }
     }
     __syncthreads();
-    // 3: placement in index order
-#pragma unroll
+    // 3: placement in index order, one load group at a time (keys re-read
+    // from L1/L2): ranks first, then the record loads, then the stores
+#pragma unroll 1
     for (int r0 = 0; r0 < kRounds; r0 += kGroup) {
-        double4 v[kGroup];
-        if (rec2) {
+        int kg[kGroup], pos[kGroup];
 #pragma unroll
-            for (int u = 0; u < kGroup; ++u) {
-                const int64_t i = wbase + (r0 + u) * 32 + lane;
-                if (kreg[r0 + u] >= 0)
-                    v[u] = make_double4(__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1),
-                                        __ldg(xyz + 3 * i + 2), __ldg(q + i));
-            }
+        for (int u = 0; u < kGroup; ++u) {
+            const int64_t i = wbase + (r0 + u) * 32 + lane;
+            kg[u] = i < n ? __ldg(key + i) : -1;
         }
 #pragma unroll
         for (int u = 0; u < kGroup; ++u) {
-            const int r = r0 + u;
-            const int k = kreg[r];
+            const int k = kg[u];
             const bool act = k >= 0;
-            const int col = act ? k / K2 : -1 - lane;
-            const unsigned peers = warp_peers<CB>(col);
-            if (act) {
-                const int pos = wc[w * ncol + col] + __popc(peers & ((1u << lane) - 1));
-                kz2[pos] = make_int2((int)(wbase + r * 32 + lane), k - col * K2);
-                if (rec2) rec2[pos] = v[u];
-            }
+            const int col = act ? k >> 16 : -1 - lane;
+            const unsigned peers = pm[w][r0 + u][lane];
+            int base = 0;
+            if (act) base = wc[w * ncol + col];
+            pos[u] = base + __popc(peers & ((1u << lane) - 1));
             __syncwarp();
-            if (act && lane == __ffs(peers) - 1) wc[w * ncol + col] += __popc(peers);
+            if (act && lane == __ffs(peers) - 1) wc[w * ncol + col] = base + __popc(peers);
             __syncwarp();
+        }
+#pragma unroll
+        for (int u = 0; u < kGroup; ++u) {
+            const int k = kg[u];
+            if (k < 0) continue;
+            const int64_t i = wbase + (r0 + u) * 32 + lane;
+            kz2[pos[u]] = make_int2((int)i, k & 0xffff);
+            if (rec2)
+                st_rec(rec2 + pos[u], make_double4(__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1),
+                                                   __ldg(xyz + 3 * i + 2), __ldg(q + i)));
         }
     }
 }
@@ -279,12 +296,159 @@ struct ZLayout {
     }
 };
 
+// Bulk (TMA) global -> shared copies completing on an mbarrier.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+// bytes is a multiple of 16; pieces of at most 32 KB
+__device__ __forceinline__ void bulk_g2s_pieces(void* dst, const void* src, unsigned bytes,
+                                                uint64_t* bar) {
+    for (unsigned o = 0; o < bytes; o += 32768u)
+        bulk_g2s(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                 min(32768u, bytes - o), bar);
+}
+
+// Whole-column variant: columns of up to kZCap particles are staged in shared
+// memory in one go (records, (index, c2) pairs, inverse permutation), ranked
+// with two ballot passes and written out in cell order as one contiguous run.
+constexpr int kZCap = 2560;
+struct ZWholeLayout {
+    size_t rec, kz, inv, cnt, zst, total;
+    __host__ __device__ ZWholeLayout(int K2, bool with_rec) {
+        rec = 0;
+        kz = with_rec ? sizeof(double4) * kZCap : 0;
+        inv = kz + sizeof(int2) * (kZCap + 2);
+        cnt = inv + sizeof(uint16_t) * kZCap;
+        cnt = (cnt + 15) & ~size_t(15);
+        zst = cnt + sizeof(int32_t) * kZWarps * K2;
+        total = zst + sizeof(int32_t) * (K2 + 1);
+    }
+};
+
+template <int ZB>
+__device__ __forceinline__ void z_sort_whole(int K2, int ncol, int col, int cs, int m, int64_t n,
+                                             const int2* __restrict__ kz2,
+                                             const double4* __restrict__ rec2,
+                                             int32_t* __restrict__ perm,
+                                             int32_t* __restrict__ start,
+                                             double4* __restrict__ sp, unsigned char* zsm,
+                                             uint64_t* bar) {
+    const ZWholeLayout L(K2, sp != nullptr);
+    double4* s_rec = reinterpret_cast<double4*>(zsm + L.rec);
+    int2* s_kz = reinterpret_cast<int2*>(zsm + L.kz);
+    uint16_t* s_inv = reinterpret_cast<uint16_t*>(zsm + L.inv);
+    int32_t* cnt = reinterpret_cast<int32_t*>(zsm + L.cnt);  // [K2][kZWarps]
+    int32_t* zst = reinterpret_cast<int32_t*>(zsm + L.zst);
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, nt = blockDim.x;
+    // 1: stage the column with bulk copies (the pair array from the even index
+    // at or below cs, so both ends are 16-byte aligned; kz2 has 2 spare slots)
+    const int cs_al = cs & ~1, m_al = ((cs + m + 1) & ~1) - cs_al;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        const unsigned brec = sp ? 32u * (unsigned)m : 0u, bkz = 8u * (unsigned)m_al;
+        mbar_expect_tx(bar, brec + bkz);
+        if (brec) bulk_g2s_pieces(s_rec, rec2 + cs, brec, bar);
+        if (bkz) bulk_g2s_pieces(s_kz, kz2 + cs_al, bkz, bar);
+    }
+    for (int e = tid; e < kZWarps * K2; e += nt) cnt[e] = 0;
+    __syncthreads();  // barrier initialised before anyone waits on it
+    mbar_wait(bar, 0);
+    s_kz += cs - cs_al;
+    // 2: per-warp counts over the warp's contiguous slice, in particle order
+    const int per = (m + kZWarps - 1) / kZWarps;
+    const int lo = min(m, w * per), hi = min(m, lo + per);
+    for (int j0 = lo; j0 < hi; j0 += 32) {
+        const int j = j0 + lane;
+        const int z = j < hi ? s_kz[j].y : -1 - lane;
+        const unsigned peers = warp_peers<ZB>(z);
+        if (z >= 0 && lane == __ffs(peers) - 1) cnt[z * kZWarps + w] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // 3: offsets in (c2, warp) order; cell starts
+    if (w == 0) {
+        int carry = 0;
+        for (int z0 = 0; z0 < K2; z0 += 32) {
+            const int z = z0 + lane;
+            int own = 0;
+            if (z < K2) {
+#pragma unroll
+                for (int k = 0; k < kZWarps; ++k) {
+                    const int t = cnt[z * kZWarps + k];
+                    cnt[z * kZWarps + k] = own;
+                    own += t;
+                }
+            }
+            int x = own;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (z < K2) {
+                const int ex = carry + x - own;
+                zst[z] = ex;
+                start[(int64_t)col * K2 + z] = cs + ex;
+#pragma unroll
+                for (int k = 0; k < kZWarps; ++k) cnt[z * kZWarps + k] += ex;
+            }
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (col == ncol - 1 && lane == 0) start[(int64_t)ncol * K2] = (int)n;
+    }
+    __syncthreads();
+    // 4: stable ranks -> inverse permutation
+    for (int j0 = lo; j0 < hi; j0 += 32) {
+        const int j = j0 + lane;
+        const int z = j < hi ? s_kz[j].y : -1 - lane;
+        const unsigned peers = warp_peers<ZB>(z);
+        int base = 0;
+        if (z >= 0) {
+            base = cnt[z * kZWarps + w];
+            s_inv[base + __popc(peers & ((1u << lane) - 1))] = (uint16_t)j;
+        }
+        __syncwarp();
+        if (z >= 0 && lane == __ffs(peers) - 1) cnt[z * kZWarps + w] = base + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // 5: the column leaves in cell order as one contiguous run
+    for (int k = tid; k < m; k += nt) {
+        const int j = s_inv[k];
+        perm[cs + k] = s_kz[j].x;
+        if (sp) st_rec(sp + cs + k, s_rec[j]);
+    }
+}
+
 // One CTA per column: stable counting sort of the column segment by c2. The
 // segment is taken kZChunk elements at a time (warp w owns a contiguous
 // kZRounds x 32 slice of the chunk); each chunk is ranked into shared memory in
 // (c2, particle) order and written out as contiguous per-cell runs.
 template <int ZB>
-__global__ void __launch_bounds__(kZWarps * 32, 3) k_z_sort(Geometry g,
+__global__ void __launch_bounds__(kZWarps * 32, 2) k_z_sort(Geometry g,
                                                          const int32_t* __restrict__ ctot,
                                                          int64_t n,
                                                          const int2* __restrict__ kz2,
@@ -295,6 +459,7 @@ __global__ void __launch_bounds__(kZWarps * 32, 3) k_z_sort(Geometry g,
     extern __shared__ __align__(16) unsigned char zsm[];
     __shared__ int32_t wsum[32];
     __shared__ int32_t red[kZWarps];
+    __shared__ uint64_t zbar;
     const int K2 = g.K[2], ncol = g.K[0] * g.K[1];
     const ZLayout L(K2, sp != nullptr);
     double4* s_rec = reinterpret_cast<double4*>(zsm + L.rec);
@@ -315,6 +480,10 @@ __global__ void __launch_bounds__(kZWarps * 32, 3) k_z_sort(Geometry g,
     int cs = 0;
     for (int k = 0; k < kZWarps; ++k) cs += red[k];
     const int m = ctot[col];
+    if (m <= kZCap) {  // uniform per CTA
+        z_sort_whole<ZB>(K2, ncol, col, cs, m, n, kz2, rec2, perm, start, sp, zsm, &zbar);
+        return;
+    }
     const int2* seg = kz2 + cs;
     // column histogram over c2 (order-free)
     for (int j0 = 0; j0 < m; j0 += 4 * kZWarps * 32) {
@@ -359,30 +528,41 @@ __global__ void __launch_bounds__(kZWarps * 32, 3) k_z_sort(Geometry g,
             int2 kz = act ? seg[c0 + jl] : make_int2(0, -1 - lane);
             zr[u] = kz.y;
             ir[u] = kz.x;
-            if (sp && act) v[u] = rec2[cs + c0 + jl];
+            if (sp && act) v[u] = ld_rec(rec2 + cs + c0 + jl);
         }
         __syncthreads();
+        unsigned pk[kZRounds];
 #pragma unroll
         for (int u = 0; u < kZRounds; ++u) {
             const unsigned peers = warp_peers<ZB>(zr[u]);
+            pk[u] = peers;
             if (zr[u] >= 0 && lane == __ffs(peers) - 1) cnt[zr[u] * kZWarps + w] += __popc(peers);
             __syncwarp();
         }
         __syncthreads();
-        if (w == 0) {  // exclusive scan in (c2, warp) order; chunk-local cell starts
+        if (w == 0) {  // exclusive offsets in (c2, warp) order; chunk-local cell starts
             int carry = 0;
-            const int E = K2 * kZWarps;
-            for (int base = 0; base < E; base += 32) {
-                const int e = base + lane;
-                const int own = e < E ? cnt[e] : 0;
+            for (int z0 = 0; z0 < K2; z0 += 32) {
+                const int z = z0 + lane;
+                int own = 0;
+                if (z < K2) {
+#pragma unroll
+                    for (int k = 0; k < kZWarps; ++k) {
+                        const int t = cnt[z * kZWarps + k];
+                        cnt[z * kZWarps + k] = own;
+                        own += t;
+                    }
+                }
                 int x = own;
                 for (int o = 1; o < 32; o <<= 1) {
                     const int y = __shfl_up_sync(0xffffffffu, x, o);
                     if (lane >= o) x += y;
                 }
-                if (e < E) {
-                    cnt[e] = carry + x - own;
-                    if (e % kZWarps == 0) lstart[e / kZWarps] = carry + x - own;
+                if (z < K2) {
+                    const int ex = carry + x - own;
+                    lstart[z] = ex;
+#pragma unroll
+                    for (int k = 0; k < kZWarps; ++k) cnt[z * kZWarps + k] += ex;
                 }
                 carry += __shfl_sync(0xffffffffu, x, 31);
             }
@@ -392,15 +572,17 @@ __global__ void __launch_bounds__(kZWarps * 32, 3) k_z_sort(Geometry g,
 #pragma unroll
         for (int u = 0; u < kZRounds; ++u) {
             const bool act = zr[u] >= 0;
-            const unsigned peers = warp_peers<ZB>(zr[u]);
+            const unsigned peers = pk[u];
+            int base = 0;
             if (act) {
-                const int lp = cnt[zr[u] * kZWarps + w] + __popc(peers & ((1u << lane) - 1));
+                base = cnt[zr[u] * kZWarps + w];
+                const int lp = base + __popc(peers & ((1u << lane) - 1));
                 s_idx[lp] = ir[u];
                 s_z[lp] = (uint16_t)zr[u];
                 if (sp) s_rec[lp] = v[u];
             }
             __syncwarp();
-            if (act && lane == __ffs(peers) - 1) cnt[zr[u] * kZWarps + w] += __popc(peers);
+            if (act && lane == __ffs(peers) - 1) cnt[zr[u] * kZWarps + w] = base + __popc(peers);
             __syncwarp();
         }
         __syncthreads();
@@ -408,7 +590,7 @@ __global__ void __launch_bounds__(kZWarps * 32, 3) k_z_sort(Geometry g,
             const int z = s_z[k];
             const int gp = zrun[z] + (k - lstart[z]);
             perm[gp] = s_idx[k];
-            if (sp) sp[gp] = s_rec[k];
+            if (sp) st_rec(sp + gp, s_rec[k]);
         }
         __syncthreads();
         for (int z = tid; z < K2; z += blockDim.x) zrun[z] += lstart[z + 1] - lstart[z];
@@ -434,8 +616,9 @@ auto pick_bits(int b, F f) {
 
 bool sort2_supported(const Geometry& g) {
     const int ncol = g.K[0] * g.K[1];
-    return (size_t)(kTileWarps * ncol + ncol + 1) * sizeof(int32_t) <= 160 * 1024 &&
-           ZLayout(g.K[2], true).total <= 160 * 1024 && ncol <= 65536 && g.K[2] <= 65536;
+    return ncol <= 32768 && (size_t)(kTileWarps * ncol + ncol + 1) * sizeof(int32_t) <= 160 * 1024 &&
+           ZLayout(g.K[2], true).total <= 160 * 1024 &&
+           ZWholeLayout(g.K[2], true).total <= 160 * 1024 && ncol <= 65536 && g.K[2] <= 65536;
 }
 
 size_t sort2_hist_entries(const Geometry& g, int64_t cap) {
@@ -484,7 +667,9 @@ void launch_sort2(const Geometry& g, int64_t n, const double* xyz, const SortBuf
         KB_CHECK_LAUNCH();
         ++l;
     }
-    z_kernel<<<ncol, kZWarps * 32, ZLayout(g.K[2], sp != nullptr).total, s>>>(
+    const size_t zsmem = std::max(ZLayout(g.K[2], sp != nullptr).total,
+                                  ZWholeLayout(g.K[2], sp != nullptr).total);
+    z_kernel<<<ncol, kZWarps * 32, zsmem, s>>>(
         g, b.ctot, n, b.kz2, b.rec, b.perm, b.start, sp);
     KB_CHECK_LAUNCH();
     ++l;

@@ -17,7 +17,11 @@ h = rows[hk]
 ex = h.index("Instructions Executed")
 si = next(i for i, x in enumerate(h) if "Warp Stall Sampling (All" in x)
 agg = {}
-num = lambda x: float(x) if x not in ("", "-") else 0.0
+def num(x):
+    try:
+        return float(x)
+    except ValueError:
+        return 0.0
 for r in rows[hk + 1:]:
     if len(r) > ex and r[0].isdigit():  # source-line rows carry the per-line aggregates
         a = agg.setdefault((int(r[0]), r[1]), [0.0, 0.0])

@@ -73,7 +73,9 @@ struct SortBuffers {
     // two-level counting sort (sort2.cu)
     int32_t* hist;        // [ncol * ntiles] per-tile column histogram, then its scan
     int32_t* ctot;        // [ncol] column totals
-    int2* kz2;            // [n] column-ordered (particle index, c2)
+    int32_t* cbase;       // [ncol + 1] column starts
+    unsigned* ticket;     // [1] last-CTA counter of k_col_scan (zero between launches)
+    int32_t* idx2;        // [n + 4] column-ordered particle indices
     int32_t* big;         // [ncell] cells too large for the warp sorter
     int32_t* nbig;        // [1]
     unsigned long long* bad;  // [2]: lowest out-of-box index, out-of-cell flag

@@ -404,7 +404,10 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, in
                 const size_t E = kb::sort2_hist_entries(g, p->cap);
                 p->sb.hist = p->alloc<int32_t>(E);
                 p->sb.ctot = p->alloc<int32_t>((size_t)g.K[0] * g.K[1]);
-                p->sb.kz2 = p->alloc<int2>(p->cap + 2);  // +2: 16-byte aligned bulk reads
+                p->sb.cbase = p->alloc<int32_t>((size_t)g.K[0] * g.K[1] + 1);
+                p->sb.ticket = p->alloc<unsigned>(1);
+                KB_CUDA(cudaMemsetAsync(p->sb.ticket, 0, sizeof(unsigned), p->stream));
+                p->sb.idx2 = p->alloc<int32_t>(p->cap + 4);  // +4: 16-byte aligned bulk reads
             }
             p->sb.perm = p->alloc<int32_t>(p->cap);
             p->sb.big = p->alloc<int32_t>(g.ncell);

@@ -131,40 +131,9 @@ __global__ void __launch_bounds__(kHistThreads) k_tile_hist(Geometry g, int64_t 
     for (int c = threadIdx.x; c < ncol; c += blockDim.x) hist[(int64_t)c * ntiles + blockIdx.x] = h[c];
 }
 
-// Warp per column: exclusive scan of hist[col][0..ntiles) in place, column
-// total to ctot[col]. Loads are issued kScanBatch x 32 at a time.
-constexpr int kScanBatch = 8;
-__global__ void __launch_bounds__(256) k_col_scan(int ncol, int ntiles, int32_t* __restrict__ hist,
-                                                  int32_t* __restrict__ ctot) {
-    const int col = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (col >= ncol) return;
-    int32_t* row = hist + (int64_t)col * ntiles;
-    int carry = 0;
-    for (int b0 = 0; b0 < ntiles; b0 += 32 * kScanBatch) {
-        int v[kScanBatch];
-#pragma unroll
-        for (int u = 0; u < kScanBatch; ++u) {
-            const int t = b0 + u * 32 + lane;
-            v[u] = t < ntiles ? row[t] : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < kScanBatch; ++u) {
-            int x = v[u];
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            const int t = b0 + u * 32 + lane;
-            if (t < ntiles) row[t] = carry + x - v[u];
-            carry += __shfl_sync(0xffffffffu, x, 31);
-        }
-    }
-    if (lane == 0) ctot[col] = carry;
-}
-
-// Exclusive scan of ctot[0..ncol) into shared memory out[0..ncol], out[ncol] =
-// total; whole CTA (blockDim a multiple of 32, <= 1024); ends synchronised.
-__device__ void block_col_bases(const int32_t* __restrict__ ctot, int ncol, int32_t* out,
+// Exclusive scan of ctot[0..ncol) into out[0..ncol], out[ncol] = total; whole
+// CTA (blockDim a multiple of 32, <= 1024); ends synchronised.
+__device__ void block_col_bases(const int32_t* ctot, int ncol, int32_t* out,
                                 int32_t* wsum /* [32] */) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nt = blockDim.x;
     const int per = (ncol + nt - 1) / nt;
@@ -196,6 +165,51 @@ __device__ void block_col_bases(const int32_t* __restrict__ ctot, int ncol, int3
     __syncthreads();
 }
 
+// Warp per column: exclusive scan of hist[col][0..ntiles) in place, column
+// total to ctot[col]. Loads are issued kScanBatch x 32 at a time. The last CTA
+// to finish (ticket counter, reset for the next launch) turns the totals into
+// the column bases cbase[0..ncol] -- a fixed-order scan, so deterministic.
+constexpr int kScanBatch = 8;
+__global__ void __launch_bounds__(256) k_col_scan(int ncol, int ntiles, int32_t* __restrict__ hist,
+                                                  int32_t* ctot, int32_t* cbase,
+                                                  unsigned* ticket) {
+    __shared__ int32_t wsum[32];
+    __shared__ bool last;
+    const int col = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (col < ncol) {
+        int32_t* row = hist + (int64_t)col * ntiles;
+        int carry = 0;
+        for (int b0 = 0; b0 < ntiles; b0 += 32 * kScanBatch) {
+            int v[kScanBatch];
+#pragma unroll
+            for (int u = 0; u < kScanBatch; ++u) {
+                const int t = b0 + u * 32 + lane;
+                v[u] = t < ntiles ? row[t] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < kScanBatch; ++u) {
+                int x = v[u];
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                const int t = b0 + u * 32 + lane;
+                if (t < ntiles) row[t] = carry + x - v[u];
+                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
+        }
+        if (lane == 0) ctot[col] = carry;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    block_col_bases(ctot, ncol, cbase, wsum);
+    if (threadIdx.x == 0) *ticket = 0u;
+}
+
 // Stable scatter by column. Warp w of tile t owns particles
 // [t*kTile + w*kRounds*32, +kRounds*32), processed 32 at a time in index order.
 // The warp's keys are loaded into registers once and the record loads of
@@ -204,16 +218,14 @@ template <int CB>
 __global__ void __launch_bounds__(kTileWarps * 32, 4) k_col_scatter(Geometry g, int64_t n, int ntiles,
                                                                  const int32_t* __restrict__ key,
                                                                  const int32_t* __restrict__ cscan,
-                                                                 const int32_t* __restrict__ ctot,
+                                                                 const int32_t* __restrict__ cbase,
                                                                  const double* __restrict__ xyz,
                                                                  const double* __restrict__ q,
-                                                                 int2* __restrict__ kz2,
+                                                                 int32_t* __restrict__ idx2,
                                                                  double4* __restrict__ rec2) {
     extern __shared__ int32_t wc[];  // [kTileWarps][ncol] per-warp column counters, then bases
-    __shared__ int32_t wsum[32];
     __shared__ unsigned pm[kTileWarps][kRounds][32];  // phase-1 peer masks, reused in phase 3
     const int ncol = g.K[0] * g.K[1];
-    int32_t* cbase = wc + kTileWarps * ncol;  // [ncol + 1]
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int e = threadIdx.x; e < kTileWarps * ncol; e += blockDim.x) wc[e] = 0;
     const int64_t wbase = (int64_t)blockIdx.x * kTile + w * (kRounds * 32);
@@ -223,7 +235,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, 4) k_col_scatter(Geometry g, 
         const int64_t i = wbase + r * 32 + lane;
         kreg[r] = i < n ? __ldg(key + i) : -1;
     }
-    block_col_bases(ctot, ncol, cbase, wsum);  // also orders the zeroing above
+    __syncthreads();
     // 1: per-warp column counts
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
@@ -273,30 +285,21 @@ __global__ void __launch_bounds__(kTileWarps * 32, 4) k_col_scatter(Geometry g, 
             const int k = kg[u];
             if (k < 0) continue;
             const int64_t i = wbase + (r0 + u) * 32 + lane;
-            kz2[pos[u]] = make_int2((int)i, k & 0xffff);
-            if (rec2)
-                st_rec(rec2 + pos[u], make_double4(__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1),
-                                                   __ldg(xyz + 3 * i + 2), __ldg(q + i)));
+            idx2[pos[u]] = (int32_t)i;
+            st_rec(rec2 + pos[u], make_double4(__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1),
+                                               __ldg(xyz + 3 * i + 2), q ? __ldg(q + i) : 0.0));
         }
     }
 }
 
-// Shared-memory layout of k_z_sort (bytes), for K2 cells per column.
-struct ZLayout {
-    size_t rec, idx, z, cnt, zrun, lstart, total;
-    __host__ __device__ ZLayout(int K2, bool with_rec) {
-        rec = 0;
-        idx = with_rec ? sizeof(double4) * kZChunk : 0;
-        z = idx + sizeof(int32_t) * kZChunk;
-        cnt = z + sizeof(uint16_t) * kZChunk;
-        cnt = (cnt + 15) & ~size_t(15);
-        zrun = cnt + sizeof(int32_t) * kZWarps * K2;
-        lstart = zrun + sizeof(int32_t) * K2;
-        total = lstart + sizeof(int32_t) * (K2 + 1);
-    }
-};
-
 // Bulk (TMA) global -> shared copies completing on an mbarrier.
+#ifdef ZSORT_PROFILE
+__device__ __forceinline__ unsigned __smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+#endif
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -332,171 +335,194 @@ __device__ __forceinline__ void bulk_g2s_pieces(void* dst, const void* src, unsi
                  min(32768u, bytes - o), bar);
 }
 
-// Whole-column variant: columns of up to kZCap particles are staged in shared
-// memory in one go (records, (index, c2) pairs, inverse permutation), ranked
-// with two ballot passes and written out in cell order as one contiguous run.
-constexpr int kZCap = 2560;
+// c2 of a staged particle record: the same exact arithmetic as the key.
+__device__ __forceinline__ int rec_c2(const Geometry& g, const double4& r) {
+    return axis_cell2(r.z, g.center[2], g.radius, g.K[2], __dmul_rn(2.0, g.radius), g.inv_diam);
+}
+
+// Whole-column variant: a column of up to kZCap particles is staged in shared
+// memory in one go (records and indices, by bulk copies), ranked with
+// per-thread counters (thread t owns a contiguous slice of the column; the
+// [c2][thread] counters are scanned in that order, which is exactly stable
+// order) and written out in cell order as one contiguous run.
+constexpr int kZCap = 2560;  // <= 10 particles per thread (4-bit counters)
+constexpr int kZThreads = kZWarps * 32;
 struct ZWholeLayout {
-    size_t rec, kz, inv, cnt, zst, total;
-    __host__ __device__ ZWholeLayout(int K2, bool with_rec) {
+    size_t rec, idx, inv, z, cnt, total;
+    __host__ __device__ explicit ZWholeLayout(int K2) {
         rec = 0;
-        kz = with_rec ? sizeof(double4) * kZCap : 0;
-        inv = kz + sizeof(int2) * (kZCap + 2);
-        cnt = inv + sizeof(uint16_t) * kZCap;
+        idx = sizeof(double4) * kZCap;
+        inv = idx + sizeof(int32_t) * (kZCap + 4);
+        z = inv + sizeof(uint16_t) * kZCap;
+        cnt = z + sizeof(uint8_t) * kZCap;
         cnt = (cnt + 15) & ~size_t(15);
-        zst = cnt + sizeof(int32_t) * kZWarps * K2;
-        total = zst + sizeof(int32_t) * (K2 + 1);
+        total = cnt + sizeof(uint16_t) * (size_t)K2 * kZThreads;
     }
 };
+constexpr size_t kZWholeMaxSmem = 112 * 1024;  // two CTAs per SM
 
 template <int ZB>
-__device__ __forceinline__ void z_sort_whole(int K2, int ncol, int col, int cs, int m, int64_t n,
-                                             const int2* __restrict__ kz2,
+__device__ __forceinline__ void z_sort_whole(const Geometry& g, int col, int cs, int m,
+                                             int64_t n, const int32_t* __restrict__ idx2,
                                              const double4* __restrict__ rec2,
                                              int32_t* __restrict__ perm,
                                              int32_t* __restrict__ start,
                                              double4* __restrict__ sp, unsigned char* zsm,
-                                             uint64_t* bar) {
-    const ZWholeLayout L(K2, sp != nullptr);
+                                             uint64_t* bar, int32_t* wsum) {
+    const int K2 = g.K[2], ncol = g.K[0] * g.K[1];
+    const ZWholeLayout L(K2);
     double4* s_rec = reinterpret_cast<double4*>(zsm + L.rec);
-    int2* s_kz = reinterpret_cast<int2*>(zsm + L.kz);
+    int32_t* s_idx = reinterpret_cast<int32_t*>(zsm + L.idx);
     uint16_t* s_inv = reinterpret_cast<uint16_t*>(zsm + L.inv);
-    int32_t* cnt = reinterpret_cast<int32_t*>(zsm + L.cnt);  // [K2][kZWarps]
-    int32_t* zst = reinterpret_cast<int32_t*>(zsm + L.zst);
-    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, nt = blockDim.x;
-    // 1: stage the column with bulk copies (the pair array from the even index
-    // at or below cs, so both ends are 16-byte aligned; kz2 has 2 spare slots)
-    const int cs_al = cs & ~1, m_al = ((cs + m + 1) & ~1) - cs_al;
+    uint8_t* s_z = reinterpret_cast<uint8_t*>(zsm + L.z);
+    uint16_t* cnt = reinterpret_cast<uint16_t*>(zsm + L.cnt);  // [K2][kZThreads]
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+#ifdef ZSORT_PROFILE
+    long long T[8];
+    int nT = 0;
+    T[nT++] = clock64();
+#define ZSTAMP() T[nT++] = clock64()
+#else
+#define ZSTAMP()
+#endif
+    // 1: stage the column with bulk copies (indices from the multiple of 4 at
+    // or below cs, so both ends are 16-byte aligned; idx2 has 4 spare slots)
+    const int cs_al = cs & ~3, m_al = ((cs + m + 3) & ~3) - cs_al;
     if (tid == 0) {
         mbar_init(bar, 1);
-        const unsigned brec = sp ? 32u * (unsigned)m : 0u, bkz = 8u * (unsigned)m_al;
-        mbar_expect_tx(bar, brec + bkz);
+        const unsigned brec = 32u * (unsigned)m, bidx = 4u * (unsigned)m_al;
+        mbar_expect_tx(bar, brec + bidx);
         if (brec) bulk_g2s_pieces(s_rec, rec2 + cs, brec, bar);
-        if (bkz) bulk_g2s_pieces(s_kz, kz2 + cs_al, bkz, bar);
+        if (bidx) bulk_g2s_pieces(s_idx, idx2 + cs_al, bidx, bar);
     }
-    for (int e = tid; e < kZWarps * K2; e += nt) cnt[e] = 0;
+    for (int e = tid; e < K2 * kZThreads; e += kZThreads) cnt[e] = 0;
     __syncthreads();  // barrier initialised before anyone waits on it
     mbar_wait(bar, 0);
-    s_kz += cs - cs_al;
-    // 2: per-warp counts over the warp's contiguous slice, in particle order
-    const int per = (m + kZWarps - 1) / kZWarps;
-    const int lo = min(m, w * per), hi = min(m, lo + per);
-    for (int j0 = lo; j0 < hi; j0 += 32) {
-        const int j = j0 + lane;
-        const int z = j < hi ? s_kz[j].y : -1 - lane;
-        const unsigned peers = warp_peers<ZB>(z);
-        if (z >= 0 && lane == __ffs(peers) - 1) cnt[z * kZWarps + w] += __popc(peers);
-        __syncwarp();
+    ZSTAMP();
+    s_idx += cs - cs_al;
+    // 2: per-thread counts over the thread's contiguous slice, kept as 4-bit
+    // counters packed in registers (at most 10 particles per thread)
+    // four named 64-bit words of 16 counters (c2 < 64); named, not an
+    // array, so they stay in registers
+    static_assert(ZB <= 6, "whole-column path handles up to 64 cells per column");
+    const int per = (m + kZThreads - 1) / kZThreads;
+    const int lo = min(m, tid * per), hi = min(m, lo + per);
+    unsigned long long n0 = 0, n1 = 0, n2 = 0, n3 = 0;
+    for (int j = lo; j < hi; ++j) {
+        const int z = rec_c2(g, s_rec[j]);
+        s_z[j] = (uint8_t)z;
+        const unsigned long long inc = 1ull << ((z & 15) * 4);
+        const int wq = z >> 4;
+        n0 += wq == 0 ? inc : 0ull;
+        n1 += wq == 1 ? inc : 0ull;
+        n2 += wq == 2 ? inc : 0ull;
+        n3 += wq == 3 ? inc : 0ull;
     }
-    __syncthreads();
-    // 3: offsets in (c2, warp) order; cell starts
-    if (w == 0) {
-        int carry = 0;
-        for (int z0 = 0; z0 < K2; z0 += 32) {
-            const int z = z0 + lane;
-            int own = 0;
-            if (z < K2) {
 #pragma unroll
-                for (int k = 0; k < kZWarps; ++k) {
-                    const int t = cnt[z * kZWarps + k];
-                    cnt[z * kZWarps + k] = own;
-                    own += t;
-                }
-            }
-            int x = own;
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (z < K2) {
-                const int ex = carry + x - own;
-                zst[z] = ex;
-                start[(int64_t)col * K2 + z] = cs + ex;
-#pragma unroll
-                for (int k = 0; k < kZWarps; ++k) cnt[z * kZWarps + k] += ex;
-            }
-            carry += __shfl_sync(0xffffffffu, x, 31);
-        }
-        if (col == ncol - 1 && lane == 0) start[(int64_t)ncol * K2] = (int)n;
+    for (int r = 0; r < 16; ++r) {
+        if (r < K2) cnt[r * kZThreads + tid] = (uint16_t)((n0 >> (4 * r)) & 15u);
+        if (16 + r < K2) cnt[(16 + r) * kZThreads + tid] = (uint16_t)((n1 >> (4 * r)) & 15u);
+        if (32 + r < K2) cnt[(32 + r) * kZThreads + tid] = (uint16_t)((n2 >> (4 * r)) & 15u);
+        if (48 + r < K2) cnt[(48 + r) * kZThreads + tid] = (uint16_t)((n3 >> (4 * r)) & 15u);
     }
     __syncthreads();
-    // 4: stable ranks -> inverse permutation
-    for (int j0 = lo; j0 < hi; j0 += 32) {
-        const int j = j0 + lane;
-        const int z = j < hi ? s_kz[j].y : -1 - lane;
-        const unsigned peers = warp_peers<ZB>(z);
-        int base = 0;
-        if (z >= 0) {
-            base = cnt[z * kZWarps + w];
-            s_inv[base + __popc(peers & ((1u << lane) - 1))] = (uint16_t)j;
+    ZSTAMP();
+    // 3: exclusive scan of the counters in (c2, thread) order: thread t scans
+    // the K2 consecutive entries [t*K2, (t+1)*K2)
+    {
+        uint16_t* strip = cnt + tid * K2;
+        int sum = 0;
+        for (int i = 0; i < K2; ++i) sum += strip[i];
+        int x = sum;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
-        __syncwarp();
-        if (z >= 0 && lane == __ffs(peers) - 1) cnt[z * kZWarps + w] = base + __popc(peers);
-        __syncwarp();
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        int off = 0;
+        for (int k = 0; k < w; ++k) off += wsum[k];
+        int run = off + x - sum;
+        for (int i = 0; i < K2; ++i) {
+            const int t = strip[i];
+            strip[i] = (uint16_t)run;
+            run += t;
+        }
     }
     __syncthreads();
+    ZSTAMP();
+    for (int z = tid; z < K2; z += kZThreads) start[(int64_t)col * K2 + z] = cs + cnt[z * kZThreads];
+    if (col == ncol - 1 && tid == 0) start[(int64_t)ncol * K2] = (int)n;
+    // 4: stable ranks -> inverse permutation (running 4-bit counters again)
+    n0 = n1 = n2 = n3 = 0;
+    for (int j = lo; j < hi; ++j) {
+        const int z = s_z[j];
+        const int sh = (z & 15) * 4, wq = z >> 4;
+        const unsigned long long cur = wq == 0 ? n0 : wq == 1 ? n1 : wq == 2 ? n2 : n3;
+        const int off = (int)((cur >> sh) & 15u);
+        const unsigned long long inc = 1ull << sh;
+        n0 += wq == 0 ? inc : 0ull;
+        n1 += wq == 1 ? inc : 0ull;
+        n2 += wq == 2 ? inc : 0ull;
+        n3 += wq == 3 ? inc : 0ull;
+        s_inv[cnt[z * kZThreads + tid] + off] = (uint16_t)j;
+    }
+    __syncthreads();
+    ZSTAMP();
     // 5: the column leaves in cell order as one contiguous run
-    for (int k = tid; k < m; k += nt) {
+    for (int k = tid; k < m; k += kZThreads) {
         const int j = s_inv[k];
-        perm[cs + k] = s_kz[j].x;
+        perm[cs + k] = s_idx[j];
         if (sp) st_rec(sp + cs + k, s_rec[j]);
     }
+#ifdef ZSORT_PROFILE
+    __syncthreads();
+    ZSTAMP();
+    if (tid == 0 && (col % 37 == 0))
+        printf("zsort col %d sm %d m %d: load %lld count %lld scan %lld rank %lld write %lld start %lld\n", col,
+               (int)__smid(), m, T[1] - T[0], T[2] - T[1], T[3] - T[2], T[4] - T[3], T[5] - T[4], T[0]);
+#endif
 }
 
-// One CTA per column: stable counting sort of the column segment by c2. The
-// segment is taken kZChunk elements at a time (warp w owns a contiguous
-// kZRounds x 32 slice of the chunk); each chunk is ranked into shared memory in
-// (c2, particle) order and written out as contiguous per-cell runs.
+// Chunked fallback for columns above kZCap (or grids whose counters do not
+// fit): the segment is taken kZChunk elements at a time (warp w owns a
+// contiguous kZRounds x 32 slice of the chunk); each chunk is ranked into
+// shared memory in (c2, particle) order and written out as contiguous
+// per-cell runs.
+struct ZLayout {
+    size_t rec, idx, z, cnt, zrun, lstart, total;
+    __host__ __device__ explicit ZLayout(int K2) {
+        rec = 0;
+        idx = sizeof(double4) * kZChunk;
+        z = idx + sizeof(int32_t) * kZChunk;
+        cnt = z + sizeof(uint16_t) * kZChunk;
+        cnt = (cnt + 15) & ~size_t(15);
+        zrun = cnt + sizeof(int32_t) * kZWarps * K2;
+        lstart = zrun + sizeof(int32_t) * K2;
+        total = lstart + sizeof(int32_t) * (K2 + 1);
+    }
+};
+
 template <int ZB>
-__global__ void __launch_bounds__(kZWarps * 32, 2) k_z_sort(Geometry g,
-                                                         const int32_t* __restrict__ ctot,
-                                                         int64_t n,
-                                                         const int2* __restrict__ kz2,
-                                                         const double4* __restrict__ rec2,
-                                                         int32_t* __restrict__ perm,
-                                                         int32_t* __restrict__ start,
-                                                         double4* __restrict__ sp) {
-    extern __shared__ __align__(16) unsigned char zsm[];
-    __shared__ int32_t wsum[32];
-    __shared__ int32_t red[kZWarps];
-    __shared__ uint64_t zbar;
+__device__ __forceinline__ void z_sort_chunked(const Geometry& g, int col, int cs, int m,
+                                               int64_t n, const int32_t* __restrict__ idx2,
+                                               const double4* __restrict__ rec2,
+                                               int32_t* __restrict__ perm,
+                                               int32_t* __restrict__ start,
+                                               double4* __restrict__ sp, unsigned char* zsm) {
     const int K2 = g.K[2], ncol = g.K[0] * g.K[1];
-    const ZLayout L(K2, sp != nullptr);
+    const ZLayout L(K2);
     double4* s_rec = reinterpret_cast<double4*>(zsm + L.rec);
     int32_t* s_idx = reinterpret_cast<int32_t*>(zsm + L.idx);
     uint16_t* s_z = reinterpret_cast<uint16_t*>(zsm + L.z);
     int32_t* cnt = reinterpret_cast<int32_t*>(zsm + L.cnt);  // [K2][kZWarps]
     int32_t* zrun = reinterpret_cast<int32_t*>(zsm + L.zrun);
     int32_t* lstart = reinterpret_cast<int32_t*>(zsm + L.lstart);
-    const int col = blockIdx.x, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-    (void)wsum;
-    // column start = sum of the totals of the columns before it
-    int s = 0;
-    for (int c = tid; c < col; c += blockDim.x) s += ctot[c];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) red[w] = s;
-    for (int e = tid; e < K2; e += blockDim.x) zrun[e] = 0;
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    for (int e = tid; e < K2; e += kZThreads) zrun[e] = 0;
     __syncthreads();
-    int cs = 0;
-    for (int k = 0; k < kZWarps; ++k) cs += red[k];
-    const int m = ctot[col];
-    if (m <= kZCap) {  // uniform per CTA
-        z_sort_whole<ZB>(K2, ncol, col, cs, m, n, kz2, rec2, perm, start, sp, zsm, &zbar);
-        return;
-    }
-    const int2* seg = kz2 + cs;
     // column histogram over c2 (order-free)
-    for (int j0 = 0; j0 < m; j0 += 4 * kZWarps * 32) {
-        int zz[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int j = j0 + u * kZWarps * 32 + tid;
-            zz[u] = j < m ? __ldg(&seg[j].y) : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (zz[u] >= 0) atomicAdd(&zrun[zz[u]], 1);
-    }
+    for (int j = tid; j < m; j += kZThreads) atomicAdd(&zrun[rec_c2(g, ld_rec(rec2 + cs + j))], 1);
     __syncthreads();
     if (w == 0) {  // cell starts; zrun becomes each cell's running output position
         int carry = cs;
@@ -518,17 +544,18 @@ __global__ void __launch_bounds__(kZWarps * 32, 2) k_z_sort(Geometry g,
     }
     for (int c0 = 0; c0 < m; c0 += kZChunk) {
         const int cm = min(kZChunk, m - c0);
-        for (int e = tid; e < kZWarps * K2; e += blockDim.x) cnt[e] = 0;
+        for (int e = tid; e < kZWarps * K2; e += kZThreads) cnt[e] = 0;
         int zr[kZRounds], ir[kZRounds];
         double4 v[kZRounds];
 #pragma unroll
         for (int u = 0; u < kZRounds; ++u) {
             const int jl = w * (kZRounds * 32) + u * 32 + lane;
-            const bool act = jl < cm;
-            int2 kz = act ? seg[c0 + jl] : make_int2(0, -1 - lane);
-            zr[u] = kz.y;
-            ir[u] = kz.x;
-            if (sp && act) v[u] = ld_rec(rec2 + cs + c0 + jl);
+            zr[u] = -1 - lane;
+            if (jl < cm) {
+                v[u] = ld_rec(rec2 + cs + c0 + jl);
+                ir[u] = __ldg(idx2 + cs + c0 + jl);
+                zr[u] = rec_c2(g, v[u]);
+            }
         }
         __syncthreads();
         unsigned pk[kZRounds];
@@ -579,22 +606,43 @@ __global__ void __launch_bounds__(kZWarps * 32, 2) k_z_sort(Geometry g,
                 const int lp = base + __popc(peers & ((1u << lane) - 1));
                 s_idx[lp] = ir[u];
                 s_z[lp] = (uint16_t)zr[u];
-                if (sp) s_rec[lp] = v[u];
+                s_rec[lp] = v[u];
             }
             __syncwarp();
             if (act && lane == __ffs(peers) - 1) cnt[zr[u] * kZWarps + w] = base + __popc(peers);
             __syncwarp();
         }
         __syncthreads();
-        for (int k = tid; k < cm; k += blockDim.x) {  // contiguous per-cell runs
+        for (int k = tid; k < cm; k += kZThreads) {  // contiguous per-cell runs
             const int z = s_z[k];
             const int gp = zrun[z] + (k - lstart[z]);
             perm[gp] = s_idx[k];
             if (sp) st_rec(sp + gp, s_rec[k]);
         }
         __syncthreads();
-        for (int z = tid; z < K2; z += blockDim.x) zrun[z] += lstart[z + 1] - lstart[z];
+        for (int z = tid; z < K2; z += kZThreads) zrun[z] += lstart[z + 1] - lstart[z];
     }
+}
+
+// One CTA per column: stable counting sort of the column segment by c2.
+template <int ZB>
+__global__ void __launch_bounds__(kZThreads, 2) k_z_sort(Geometry g,
+                                                       const int32_t* __restrict__ cbase,
+                                                       int64_t n, int whole_ok,
+                                                       const int32_t* __restrict__ idx2,
+                                                       const double4* __restrict__ rec2,
+                                                       int32_t* __restrict__ perm,
+                                                       int32_t* __restrict__ start,
+                                                       double4* __restrict__ sp) {
+    extern __shared__ __align__(16) unsigned char zsm[];
+    __shared__ int32_t wsum[32];
+    __shared__ uint64_t zbar;
+    const int col = blockIdx.x;
+    const int cs = __ldg(cbase + col), m = __ldg(cbase + col + 1) - cs;
+    if (ZB <= 6 && whole_ok && m <= kZCap)  // uniform per CTA
+        z_sort_whole<(ZB <= 6 ? ZB : 6)>(g, col, cs, m, n, idx2, rec2, perm, start, sp, zsm, &zbar, wsum);
+    else
+        z_sort_chunked<ZB>(g, col, cs, m, n, idx2, rec2, perm, start, sp, zsm);
 }
 
 // Instantiation for an even key width in [2, 16].
@@ -617,8 +665,7 @@ auto pick_bits(int b, F f) {
 bool sort2_supported(const Geometry& g) {
     const int ncol = g.K[0] * g.K[1];
     return ncol <= 32768 && (size_t)(kTileWarps * ncol + ncol + 1) * sizeof(int32_t) <= 160 * 1024 &&
-           ZLayout(g.K[2], true).total <= 160 * 1024 &&
-           ZWholeLayout(g.K[2], true).total <= 160 * 1024 && ncol <= 65536 && g.K[2] <= 65536;
+           ZLayout(g.K[2]).total <= 160 * 1024 && g.K[2] <= 65536;
 }
 
 size_t sort2_hist_entries(const Geometry& g, int64_t cap) {
@@ -657,20 +704,20 @@ void launch_sort2(const Geometry& g, int64_t n, const double* xyz, const SortBuf
         KB_CUDA(cudaMemsetAsync(b.hist, 0, sizeof(int32_t) * E, s));
     }
     KB_CHECK_LAUNCH();
-    k_col_scan<<<(ncol + 7) / 8, 256, 0, s>>>(ncol, ntiles, b.hist, b.ctot);
+    k_col_scan<<<(ncol + 7) / 8, 256, 0, s>>>(ncol, ntiles, b.hist, b.ctot, b.cbase, b.ticket);
     KB_CHECK_LAUNCH();
     ++l;
     if (n > 0) {
         col_kernel<<<ntiles, kTileWarps * 32, (kTileWarps * ncol + ncol + 1) * sizeof(int32_t),
-                        s>>>(g, n, ntiles, b.key, b.hist, b.ctot, xyz, q, b.kz2,
-                             sp ? b.rec : nullptr);
+                        s>>>(g, n, ntiles, b.key, b.hist, b.cbase, xyz, q, b.idx2, b.rec);
         KB_CHECK_LAUNCH();
         ++l;
     }
-    const size_t zsmem = std::max(ZLayout(g.K[2], sp != nullptr).total,
-                                  ZWholeLayout(g.K[2], sp != nullptr).total);
-    z_kernel<<<ncol, kZWarps * 32, zsmem, s>>>(
-        g, b.ctot, n, b.kz2, b.rec, b.perm, b.start, sp);
+    const size_t wsmem = ZWholeLayout(g.K[2]).total;
+    const int whole_ok = wsmem <= kZWholeMaxSmem && g.K[2] <= 64;
+    const size_t zsmem = std::max(ZLayout(g.K[2]).total, whole_ok ? wsmem : 0);
+    z_kernel<<<ncol, kZThreads, zsmem, s>>>(g, b.cbase, n, whole_ok, b.idx2, b.rec, b.perm,
+                                            b.start, sp);
     KB_CHECK_LAUNCH();
     ++l;
     if (launches) *launches += l;

@@ -438,6 +438,86 @@ __device__ __forceinline__ void zero_padding(double* As, double* Bs, int lane) {
     for (int e = lane; e < (T::NT * 8 - T::L2) * T::LDP; e += 32) Bs[T::L2 * T::LDP + e] = 0.0;
 }
 
+// Column epilogue shared by the spread kernels: cross-warp sum of the warps'
+// T1 partials (at sm + w * per_warp + t1off, [L^2][RP]), then either the fused
+// y, x contractions into this column's partial core (Fpart) or the T1 slab.
+template <int L>
+__device__ __forceinline__ void spread_epilogue(const ColumnArgs& a, const ColumnRange& cr, double* sm,
+                                                int per_warp, int t1off, double* red, double qsum,
+                                                int want_fwd) {
+    constexpr int L2 = L * L, NW = 4;
+    const Geometry& g = a.g;
+    const int R = g.R, RP = ((R + 7) / 8) * 8;
+    __syncthreads();
+    red[threadIdx.x] = qsum;
+    if (want_fwd && a.Fpart) {
+        // Fused y, x contractions: this column segment's partial core
+        //   Fcol[r0][r1][r2] = sum_{i,j} W0[r0][x_i] W1[r1][y_j] T1col[(i,j)][r2]
+        // (the V_1, V_0 phases of spkmv restricted to one column; summed over
+        // columns in order by k_core_sum).
+        double* tc = sm + NW * per_warp;    // [L^2][R]
+        double* u = tc + L2 * R;            // [L][R][R]
+        __syncthreads();
+        for (int e = threadIdx.x; e < L2 * R; e += 128) {
+            const int ij = e / R, r = e % R;
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) s += sm[w * per_warp + t1off + ij * RP + r];
+            tc[e] = s;
+        }
+        __syncthreads();
+        double* w01 = u + L * R * R;  // [2][R][L] the column's W0 / W1 rows
+        for (int e = threadIdx.x; e < R * L; e += 128) {
+            w01[e] = a.W0[(int64_t)(e / L) * g.n[0] + cr.c0 * L + e % L];
+            w01[R * L + e] = a.W1[(int64_t)(e / L) * g.n[1] + cr.c1 * L + e % L];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < L * R * R; e += 128) {
+            const int i = e / (R * R), r1 = (e / R) % R, r2 = e % R;
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < L; ++j) s = fma(w01[R * L + r1 * L + j], tc[(i * L + j) * R + r2], s);
+            u[e] = s;
+        }
+        __syncthreads();
+        // Fpart is entry-major, [R^3+1][nblocks], so k_core_sum reads it coalesced
+        const int nblocks = a.S * g.K[0] * g.K[1];
+        double* dst = a.Fpart + (int64_t)cr.seg * g.K[0] * g.K[1] + cr.col;
+        for (int e = threadIdx.x; e < R * R * R; e += 128) {
+            const int r0 = e / (R * R), rr = e % (R * R);
+            double s = 0.0;
+#pragma unroll
+            for (int i = 0; i < L; ++i) s = fma(w01[r0 * L + i], u[i * R * R + rr], s);
+            dst[(int64_t)e * nblocks] = s;
+        }
+        __syncthreads();
+        for (int o = 64; o > 0; o >>= 1) {
+            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) dst[(int64_t)R * R * R * nblocks] = red[0];
+        return;
+    }
+    if (want_fwd) {
+        double* dst = a.T1 + (int64_t)cr.seg * g.n[0] * g.n[1] * R;
+        for (int e = threadIdx.x; e < L2 * R; e += 128) {
+            const int ij = e / R, r = e % R, i = ij / L, j = ij % L;
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) s += sm[w * per_warp + t1off + ij * RP + r];
+            dst[((int64_t)(cr.c0 * L + i) * g.n[1] + cr.c1 * L + j) * R + r] = s;
+        }
+    }
+    if (a.colq) {
+        __syncthreads();
+        for (int o = 64; o > 0; o >>= 1) {
+            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) a.colq[(int64_t)cr.seg * g.K[0] * g.K[1] + cr.col] = red[0];
+    }
+}
+
 template <int L, bool MONO>
 __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, int want_fwd) {
     using T = SpreadTile<L>;
@@ -603,74 +683,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
         zero_padding<L>(As, Bs, lane);
         __syncwarp();
     }
-    __syncthreads();
-    red[threadIdx.x] = qsum;
-    if (want_fwd && a.Fpart) {
-        // Fused y, x contractions: this column segment's partial core
-        //   Fcol[r0][r1][r2] = sum_{i,j} W0[r0][x_i] W1[r1][y_j] T1col[(i,j)][r2]
-        // (the V_1, V_0 phases of spkmv restricted to one column; summed over
-        // columns in order by k_core_sum).
-        double* tc = sm + NW * per_warp;    // [L^2][R]
-        double* u = tc + L2 * R;            // [L][R][R]
-        __syncthreads();
-        for (int e = threadIdx.x; e < L2 * R; e += 128) {
-            const int ij = e / R, r = e % R;
-            double s = 0.0;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) s += sm[w * per_warp + T::stage + ij * RP + r];
-            tc[e] = s;
-        }
-        __syncthreads();
-        double* w01 = u + L * R * R;  // [2][R][L] the column's W0 / W1 rows
-        for (int e = threadIdx.x; e < R * L; e += 128) {
-            w01[e] = a.W0[(int64_t)(e / L) * g.n[0] + cr.c0 * L + e % L];
-            w01[R * L + e] = a.W1[(int64_t)(e / L) * g.n[1] + cr.c1 * L + e % L];
-        }
-        __syncthreads();
-        for (int e = threadIdx.x; e < L * R * R; e += 128) {
-            const int i = e / (R * R), r1 = (e / R) % R, r2 = e % R;
-            double s = 0.0;
-#pragma unroll
-            for (int j = 0; j < L; ++j) s = fma(w01[R * L + r1 * L + j], tc[(i * L + j) * R + r2], s);
-            u[e] = s;
-        }
-        __syncthreads();
-        // Fpart is entry-major, [R^3+1][nblocks], so k_core_sum reads it coalesced
-        const int nblocks = a.S * g.K[0] * g.K[1];
-        double* dst = a.Fpart + (int64_t)cr.seg * g.K[0] * g.K[1] + cr.col;
-        for (int e = threadIdx.x; e < R * R * R; e += 128) {
-            const int r0 = e / (R * R), rr = e % (R * R);
-            double s = 0.0;
-#pragma unroll
-            for (int i = 0; i < L; ++i) s = fma(w01[r0 * L + i], u[i * R * R + rr], s);
-            dst[(int64_t)e * nblocks] = s;
-        }
-        __syncthreads();
-        for (int o = 64; o > 0; o >>= 1) {
-            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) dst[(int64_t)R * R * R * nblocks] = red[0];
-        return;
-    }
-    if (want_fwd) {
-        double* dst = a.T1 + (int64_t)cr.seg * g.n[0] * g.n[1] * R;
-        for (int e = threadIdx.x; e < L2 * R; e += 128) {
-            const int ij = e / R, r = e % R, i = ij / L, j = ij % L;
-            double s = 0.0;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) s += sm[w * per_warp + T::stage + ij * RP + r];
-            dst[((int64_t)(cr.c0 * L + i) * g.n[1] + cr.c1 * L + j) * R + r] = s;
-        }
-    }
-    if (a.colq) {
-        __syncthreads();
-        for (int o = 64; o > 0; o >>= 1) {
-            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) a.colq[(int64_t)cr.seg * g.K[0] * g.K[1] + cr.col] = red[0];
-    }
+    spread_epilogue<L>(a, cr, sm, per_warp, T::stage, red, qsum, want_fwd);
 }
 
 // Backward z-expansion + gather with compile-time L: psi for a batch of the

@@ -423,6 +423,10 @@ struct SpreadTile {
     static_assert(MT2 * 8 * LDK <= stage, "phi must fit in the staging area");
 };
 
+__host__ __device__ constexpr int spread_epilogue_doubles(int L, int R) {
+    return L * L * R + L * R * R + 2 * R * L;
+}
+
 template <int L>
 __host__ __device__ constexpr int spread_warp_doubles(int R) {
     return SpreadTile<L>::stage + SpreadTile<L>::MT2 * 8 * ((R + 7) / 8) * 8;
@@ -441,13 +445,15 @@ __device__ __forceinline__ void zero_padding(double* As, double* Bs, int lane) {
 // Column epilogue shared by the spread kernels: cross-warp sum of the warps'
 // T1 partials (at sm + w * per_warp + t1off, [L^2][RP]), then either the fused
 // y, x contractions into this column's partial core (Fpart) or the T1 slab.
+// epi: scratch for the contractions (spread_epilogue_doubles), not
+// overlapping any warp's T1 partial.
 template <int L>
 __device__ __forceinline__ void spread_epilogue(const ColumnArgs& a, const ColumnRange& cr, double* sm,
-                                                int per_warp, int t1off, double* red, double qsum,
-                                                int want_fwd) {
+                                                int per_warp, int t1off, int RP, double* epi,
+                                                double* red, double qsum, int want_fwd) {
     constexpr int L2 = L * L, NW = 4;
     const Geometry& g = a.g;
-    const int R = g.R, RP = ((R + 7) / 8) * 8;
+    const int R = g.R;
     __syncthreads();
     red[threadIdx.x] = qsum;
     if (want_fwd && a.Fpart) {
@@ -455,7 +461,7 @@ __device__ __forceinline__ void spread_epilogue(const ColumnArgs& a, const Colum
         //   Fcol[r0][r1][r2] = sum_{i,j} W0[r0][x_i] W1[r1][y_j] T1col[(i,j)][r2]
         // (the V_1, V_0 phases of spkmv restricted to one column; summed over
         // columns in order by k_core_sum).
-        double* tc = sm + NW * per_warp;    // [L^2][R]
+        double* tc = epi;  // [L^2][R]
         double* u = tc + L2 * R;            // [L][R][R]
         __syncthreads();
         for (int e = threadIdx.x; e < L2 * R; e += 128) {
@@ -683,7 +689,270 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, i
         zero_padding<L>(As, Bs, lane);
         __syncwarp();
     }
-    spread_epilogue<L>(a, cr, sm, per_warp, T::stage, red, qsum, want_fwd);
+    spread_epilogue<L>(a, cr, sm, per_warp, T::stage, RP,
+                       spread_epilogue_doubles(L, R) <= T::stage ? sm : sm + NW * per_warp, red,
+                       qsum, want_fwd);
+}
+
+// Spread, factored-operand variant (monomial basis, L <= 8): the same
+// per-cell GEMM phi[i][n] = sum_p (q t0^i)_p B[p][n] over the L^2 pairs
+// n = (j, k), with the m8n8k4 B fragment of lane (g = lane/4, p = lane%4) at
+// n-tile t factored as B[p][8t + g] = U[p][g] * bv_p^t:
+//   g < L:   (j, k) = (g, t),                          U = t1^g,         bv = t2
+//   g >= L:  e = (g-L) NT + t, (j, k) = (e%L, NT+e/L),  U = t1^j0 t2^k,   bv = t1
+// (the k >= NT pairs; no lane's slots wrap across k for L <= 8, and lanes whose
+// only valid slot is t = 0 take bv = 0). Per 16-particle chunk a lane pair
+// stages one particle's A row (q t0^i, 8) and U row (8) plus (t1, t2) in
+// shared memory -- 18 doubles per particle instead of the 48 of k_spread_mma
+// -- and each k-step forms its B fragments in registers (5 DMUL) while the
+// tensor pipe runs the DMMAs.
+template <int L>
+struct UvMap {
+    static constexpr int L2 = L * L;
+    static constexpr int NT = (L2 + 7) / 8;
+    static constexpr int MT2 = (L2 + 7) / 8;
+    static constexpr int KS2 = (L + 3) / 4;
+    static constexpr int LDK = KS2 * 4 + 4;  // ph row stride: 2 LDK = 8 mod 16 words, conflict-free A reads
+    // (j, k) of column n = 8 t + g as j * L + k; -1 for a padding slot
+    __host__ __device__ static constexpr int pair(int g, int t) {
+        if (t >= NT) return -1;
+        if (g < L) return g * L + t;  // k = t < L since NT <= L
+        const int e = (g - L) * NT + t;
+        const int j = e % L, k = NT + e / L;
+        return k < L ? j * L + k : -1;
+    }
+    // exponents of U for lane group g (U = t1^eu1 t2^eu2; -1: U = 0)
+    __host__ __device__ static constexpr int eu1(int g) {
+        return g < L ? g : (pair(g, 0) >= 0 ? pair(g, 0) / L : -1);
+    }
+    __host__ __device__ static constexpr int eu2(int g) {
+        return g < L ? 0 : (pair(g, 0) >= 0 ? pair(g, 0) % L : -1);
+    }
+    // slots t >= 1 valid for group g (else bv = 0)
+    __host__ __device__ static constexpr bool multi(int g) { return NT > 1 && pair(g, 1) >= 0; }
+    static constexpr int stage = 16 * 8 * 2 + 16 * 2;  // A rows, U rows, (t1, t2)
+    static constexpr int ph = MT2 * 8 * LDK;
+    static constexpr int area = stage > ph ? stage : ph;
+};
+
+// T1 partial row stride: >= the padded R and = 8 mod 16 doubles, so the
+// per-cell double2 accumulate (two rows per 8-lane phase) is conflict-free.
+__host__ __device__ constexpr int uv_t1_stride(int R) {
+    return ((R + 7) / 8) * 8 % 16 == 8 ? ((R + 7) / 8) * 8 : ((R + 7) / 8) * 8 + 8;
+}
+
+template <int L>
+__host__ __device__ constexpr int spread_uv_warp_doubles(int R) {
+    return UvMap<L>::area + UvMap<L>::MT2 * 8 * uv_t1_stride(R);
+}
+
+// 16-byte-chunk XOR swizzle of an 8-double row: conflict-free 16-lane row
+// stores and 32-lane fragment reads.
+__device__ __forceinline__ int uv_swz(int row, int col) {
+    return row * 8 + ((((col >> 1) ^ (row >> 1)) & 3) << 1) + (col & 1);
+}
+
+// CTA shared memory of k_spread_uv: 4 warp areas, the column's W2 (R x n2)
+// and the epilogue scratch.
+template <int L>
+__host__ __device__ constexpr size_t spread_uv_smem_doubles(int R, int n2) {
+    return 4 * (size_t)spread_uv_warp_doubles<L>(R) + (size_t)R * n2 +
+           (size_t)spread_epilogue_doubles(L, R);
+}
+
+#ifndef UV_SKIP
+#define UV_SKIP 0  // profiling ablations only: 1 k-step loop, 2 per-cell contraction, 4 epilogue,
+                   // 8 raw per-cell fragments to a scratch buffer
+#endif
+__device__ double* uv_scratch;
+template <int L>
+__global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, int want_fwd) {
+    using M = UvMap<L>;
+    constexpr int L2 = M::L2, L3 = L2 * L, NT = M::NT, MT2 = M::MT2, KS2 = M::KS2, LDK = M::LDK;
+    constexpr int NW = 4;
+    const Geometry& g = a.g;
+    const int R = g.R, RT = (R + 7) / 8, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int RP = uv_t1_stride(R), n2 = g.n[2];
+    const ColumnRange cr = column_range(g, a.S);
+    extern __shared__ double sm[];
+    const int per_warp = spread_uv_warp_doubles<L>(R);
+    double* As = sm + warp * per_warp;  // [16][8] swizzled rows q t0^i
+    double* Us = As + 16 * 8;           // [16][8] swizzled rows U
+    double2* Ts = reinterpret_cast<double2*>(Us + 16 * 8);  // [16] (t1, t2)
+    double* ph = As;                    // [MT2*8][LDK] finished cell grid (aliases staging)
+    double* t1w = As + M::area;         // [MT2*8][RP]  warp partial of T1
+    double* w2s = sm + NW * per_warp;   // [R][n2] W2 (monomial rows), shared by the CTA
+    double* epi = w2s + R * n2;
+    __shared__ double red[128];
+    __shared__ int cst[66];             // cell starts of this column segment (+1)
+    for (int e = lane; e < MT2 * 8 * RP; e += 32) t1w[e] = 0.0;
+    for (int e0 = threadIdx.x; e0 < R * n2; e0 += 128 * 8) {  // loads in flight together
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (e0 + 128 * u < R * n2) v[u] = __ldg(a.W2 + e0 + 128 * u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (e0 + 128 * u < R * n2) w2s[e0 + 128 * u] = v[u];
+    }
+    const int col_cell0 = (cr.c0 * g.K[1] + cr.c1) * g.K[2];
+    const int nz = cr.ze - cr.zb;
+    const bool cst_ok = nz + 1 <= 66;
+    if (cst_ok)
+        for (int e = threadIdx.x; e <= nz; e += 128) cst[e] = a.start[col_cell0 + cr.zb + e];
+    const CellAxis ax0 = cell_axis_tab(a.cellax[0], cr.c0), ax1 = cell_axis_tab(a.cellax[1], cr.c1);
+    // staging role: lane pair (p, h); fragment role: (gg, tg)
+    const int p = lane & 15, h = lane >> 4;
+    const int gg = lane >> 2, tg = lane & 3;
+    const bool use_t2 = gg < L, multi = M::multi(gg);
+    unsigned long long badf = 0;
+    double qsum = 0.0;
+    __syncthreads();
+    auto cstart = [&](int c2) { return cst_ok ? cst[c2 - cr.zb] : a.start[col_cell0 + c2]; };
+
+    int zw0, zw1;
+    {
+        const int P0 = cstart(cr.zb), P1 = cstart(cr.ze);
+        const int t0 = P0 + (int)((long long)(P1 - P0) * warp / NW);
+        const int t1 = P0 + (int)((long long)(P1 - P0) * (warp + 1) / NW);
+        zw0 = warp == 0 ? cr.zb
+                        : warp_lower_bound(a.start, col_cell0 + cr.zb, col_cell0 + cr.ze, t0, lane) - col_cell0;
+        zw1 = warp == NW - 1 ? cr.ze
+                             : warp_lower_bound(a.start, col_cell0 + cr.zb, col_cell0 + cr.ze, t1, lane) - col_cell0;
+    }
+    int s_next = cstart(zw0);
+    for (int c2 = zw0; c2 < zw1; ++c2) {
+        const int s0 = s_next, s1 = cstart(c2 + 1);
+        s_next = s1;
+        if (s0 == s1) {
+            if (a.phi_cells)
+                for (int node = lane; node < L3; node += 32)
+                    a.phi_cells[(int64_t)(col_cell0 + c2) * L3 + node] = 0.0;
+            continue;
+        }
+        const CellAxis ax2 = cell_axis_tab(a.cellax[2], c2);
+        double acc[NT][2];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+        // lanes past the chunk end clamp to a valid particle and carry q = 0
+        double4 nxt = ld_rec(a.sp + s0 + min(p, s1 - s0 - 1));
+        for (int base = s0; base < s1; base += 16) {
+            const int cnt = min(16, s1 - base);
+            const double4 pt = nxt;  // software prefetch of the next chunk
+            if (base + 16 < s1) nxt = ld_rec(a.sp + base + 16 + min(p, s1 - base - 16 - 1));
+            const double q = p < cnt ? pt.w : 0.0;
+            qsum += h == 0 ? q : 0.0;
+            const double t0 = (pt.x - ax0.mid) * ax0.inv;
+            const double t1 = (pt.y - ax1.mid) * ax1.inv;
+            const double t2 = (pt.z - ax2.mid) * ax2.inv;
+            // tensor_weights' out-of-cell check, |t| <= 1 + 2e-12 (slack 1e-12 of the width)
+            badf |= fmax(fabs(t0), fmax(fabs(t1), fabs(t2))) > 1.0 + 2e-12 ? 1ull : 0ull;
+            __syncwarp();  // previous chunk's fragment reads done
+            double row[8];
+            if (h == 0) {
+                double w = q;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    row[i] = i < L ? w : 0.0;
+                    w *= t0;
+                }
+            } else {
+                double p1[L], p2[L];
+                p1[0] = p2[0] = 1.0;
+#pragma unroll
+                for (int e = 1; e < L; ++e) {
+                    p1[e] = p1[e - 1] * t1;
+                    p2[e] = p2[e - 1] * t2;
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int e1 = M::eu1(i), e2 = M::eu2(i);
+                    row[i] = e1 < 0 ? 0.0 : (e2 == 0 ? p1[e1 < 0 ? 0 : e1] : p1[e1 < 0 ? 0 : e1] * p2[e2 < 0 ? 0 : e2]);
+                }
+                Ts[p] = make_double2(t1, t2);
+            }
+            double* dst = h == 0 ? As : Us;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                *reinterpret_cast<double2*>(dst + uv_swz(p, 2 * c)) = make_double2(row[2 * c], row[2 * c + 1]);
+            __syncwarp();
+            const int ks = (UV_SKIP & 1) ? 0 : (cnt + 3) >> 2;
+            for (int kk = 0; kk < ks; ++kk) {
+                const int r = kk * 4 + tg;
+                const double2 tt = Ts[r];
+                const double af = As[uv_swz(r, gg)];
+                const double u = Us[uv_swz(r, gg)];
+                const double bv = multi ? (use_t2 ? tt.y : tt.x) : 0.0;
+                double v[NT];
+                v[0] = u;
+#pragma unroll
+                for (int t = 1; t < NT; ++t) v[t] = v[t - 1] * bv;
+#pragma unroll
+                for (int t = 0; t < NT; ++t) dmma884(acc[t], af, v[t]);
+            }
+        }
+        __syncwarp();  // staging reads done: reuse it as ph[(i,j)][k]
+        if (UV_SKIP & 8) {  // ablation: raw fragments straight to global
+            double2* o = reinterpret_cast<double2*>(uv_scratch) + ((int64_t)(col_cell0 + c2) * NT) * 32 + lane;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) o[t * 32] = make_double2(acc[t][0], acc[t][1]);
+        }
+        if (UV_SKIP & 2) continue;
+        for (int e = lane; e < MT2 * 8 * LDK; e += 32) ph[e] = 0.0;
+        __syncwarp();
+        const int i_row = lane >> 2;
+        if (i_row < L) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int jk = M::pair(2 * (lane & 3) + c, t);
+                    if (jk >= 0) ph[(i_row * L + jk / L) * LDK + jk % L] = acc[t][c];
+                }
+        }
+        __syncwarp();
+        if (a.phi_cells)
+            for (int node = lane; node < L3; node += 32)
+                a.phi_cells[(int64_t)(col_cell0 + c2) * L3 + node] = ph[(node / L) * LDK + node % L];
+        if (want_fwd) {
+            // T1c = ph[(i,j)][k] (MT2*8 x LDK) . W2s[k][r] (LDK x RP)
+            double bf[KS2][4];
+            const double* w2c = w2s + c2 * L;
+#pragma unroll
+            for (int s = 0; s < KS2; ++s)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int k = s * 4 + (lane & 3), rr = t * 8 + (lane >> 2);
+                    bf[s][t] = (t < RT && k < L && rr < R) ? w2c[rr * n2 + k] : 0.0;
+                }
+#pragma unroll
+            for (int mt = 0; mt < MT2; ++mt) {
+                double c[4][2];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) c[t][0] = c[t][1] = 0.0;
+#pragma unroll
+                for (int s = 0; s < KS2; ++s) {
+                    const double af = ph[(mt * 8 + (lane >> 2)) * LDK + s * 4 + (lane & 3)];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (t < RT) dmma884(c[t], af, bf[s][t]);
+                }
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (t < RT) {
+                        double2* d = reinterpret_cast<double2*>(t1w + (mt * 8 + (lane >> 2)) * RP + t * 8 +
+                                                                2 * (lane & 3));
+                        const double2 o = *d;
+                        *d = make_double2(o.x + c[t][0], o.y + c[t][1]);
+                    }
+            }
+        }
+        __syncwarp();
+    }
+    badf = __reduce_or_sync(0xffffffffu, (unsigned)badf);
+    if (lane == 0 && badf) atomicOr(&a.bad[1], 1ull);
+    if (UV_SKIP & 4) return;
+    spread_epilogue<L>(a, cr, sm, per_warp, M::area, RP, epi, red, qsum, want_fwd);
 }
 
 // Backward z-expansion + gather with compile-time L: psi for a batch of the
@@ -890,8 +1159,9 @@ int gather_batch(const Geometry& g) {
 template <int L, bool MONO>
 void launch_spread_mma_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
     const int R = a.g.R;
+    const bool fits = spread_epilogue_doubles(L, R) <= SpreadTile<L>::stage;
     const size_t smem = sizeof(double) * (SpreadTile<L>::NW * spread_warp_doubles<L>(R) +
-                                          (size_t)L * L * R + (size_t)L * R * R + 2 * (size_t)R * L);
+                                          (fits ? 0 : (size_t)spread_epilogue_doubles(L, R)));
     static int attr_done = 0;
     if (!attr_done) {
         KB_CUDA(cudaFuncSetAttribute(k_spread_mma<L, MONO>,
@@ -904,9 +1174,39 @@ void launch_spread_mma_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
     KB_CHECK_LAUNCH();
 }
 
+#ifndef SPREAD_UV
+#define SPREAD_UV 1
+#endif
+template <int L>
+void launch_spread_uv_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
+    const size_t smem = sizeof(double) * spread_uv_smem_doubles<L>(a.g.R, a.g.n[2]);
+    static int attr_done = 0;
+    if (!attr_done) {
+        KB_CUDA(cudaFuncSetAttribute(k_spread_uv<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+        attr_done = 1;
+    }
+    if (smem > 200 * 1024) {  // very long columns: the staged-product kernel
+        launch_spread_mma_t<L, true>(a, want_fwd, s);
+        return;
+    }
+    const int grid = a.g.K[0] * a.g.K[1] * a.S;
+    if (UV_SKIP & 8) {
+        static double* scratch = nullptr;
+        if (!scratch) {
+            KB_CUDA(cudaMalloc(&scratch, sizeof(double) * 64 * 8 * (size_t)a.g.ncell));
+            KB_CUDA(cudaMemcpyToSymbol(uv_scratch, &scratch, sizeof(scratch)));
+        }
+    }
+    k_spread_uv<L><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+    KB_CHECK_LAUNCH();
+}
+
 template <int L>
 void launch_spread_mma(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
-    if (a.mono)
+    if (a.mono && SPREAD_UV)
+        launch_spread_uv_t<L>(a, want_fwd, s);
+    else if (a.mono)
         launch_spread_mma_t<L, true>(a, want_fwd, s);
     else
         launch_spread_mma_t<L, false>(a, want_fwd, s);

@@ -373,7 +373,13 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, in
             p->form = cfg->formulation == KPME_GPU_FORM_DENSE ? KPME_GPU_FORM_DENSE
                                                               : KPME_GPU_FORM_COLLAPSED;
             const int ncol = g.K[0] * g.K[1];
-            p->S = std::max(1, std::min(std::max(1, g.z_hi - g.z_lo), (4 * 148 + ncol - 1) / ncol));
+#ifdef KPME_FORCE_S
+            p->S = KPME_FORCE_S;
+#else
+            // z segments per column: enough CTAs for one resident wave (3 per SM
+            // for the column kernels), never more than one wave
+            p->S = std::max(1, std::min(std::max(1, g.z_hi - g.z_lo), (3 * 148) / ncol));
+#endif
 
             const int P = 2 * g.M + 1;
             p->tw = p->alloc<double>(std::max(1, p->nterms));

@@ -20,6 +20,11 @@ xyz = torch.as_tensor(w.data.cloud.positions, device="cuda").contiguous()
 q = torch.as_tensor(w.data.charges.values, device="cuda").contiguous()
 out = torch.empty(w.n, dtype=torch.float64, device="cuda")
 for _ in range(reps):
-    plan.execute(xyz, q, out)
+    try:
+        plan.execute(xyz, q, out)
+    except Exception as e:  # ablation builds (-D...SKIP) compute garbage on purpose
+        if not os.environ.get("PROFILE_NOCHECK"):
+            raise
+        print("ignored:", e)
 torch.cuda.synchronize()
 print(f"{name}: ok, |z| = {float(torch.linalg.norm(out)):.6e}")

@@ -7,9 +7,9 @@ mkdir -p gpurun_out
 for flags in "$@"; do
   make -C paper_2601_18838_b200/csrc clean > /dev/null
   make -C paper_2601_18838_b200/csrc -j8 NVEXTRA="$flags" > /dev/null 2>&1 || { echo "build failed: $flags"; continue; }
-  python scripts/profile_step.py cfg3 3 > /dev/null 2>&1 || { echo "run failed: $flags"; continue; }
+  PROFILE_NOCHECK=1 python scripts/profile_step.py cfg3 3 > /dev/null 2>&1 || { echo "run failed: $flags"; continue; }
   tag=$(echo "$flags" | tr -c 'A-Za-z0-9' '_')
-  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/var_$tag.csv \
+  PROFILE_NOCHECK=1 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/var_$tag.csv \
       python scripts/profile_step.py cfg3 3 > /dev/null 2>&1
   echo "== $flags"
   python scripts/launches.py gpurun_out/var_$tag.csv | grep -E "${SWEEP_GREP:-spread|gather|keys|place|segsort}"

@@ -810,21 +810,33 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, in
     __syncthreads();
     auto cstart = [&](int c2) { return cst_ok ? cst[c2 - cr.zb] : a.start[col_cell0 + c2]; };
 
-    int zw0, zw1;
+    // Warp w takes particles [pw0, pw1), an exact quarter of the column
+    // segment; its end cells are shared with the neighbouring warps (the
+    // contraction is linear, so partial cells simply add). Stage output
+    // (phi_cells) needs whole cells: then the split is at cell boundaries.
+    int zw0, zw1, pw0, pw1;
     {
         const int P0 = cstart(cr.zb), P1 = cstart(cr.ze);
         const int t0 = P0 + (int)((long long)(P1 - P0) * warp / NW);
         const int t1 = P0 + (int)((long long)(P1 - P0) * (warp + 1) / NW);
-        zw0 = warp == 0 ? cr.zb
-                        : warp_lower_bound(a.start, col_cell0 + cr.zb, col_cell0 + cr.ze, t0, lane) - col_cell0;
-        zw1 = warp == NW - 1 ? cr.ze
-                             : warp_lower_bound(a.start, col_cell0 + cr.zb, col_cell0 + cr.ze, t1, lane) - col_cell0;
+        auto lb = [&](int target) {  // first c in [zb, ze] with cstart(c) >= target
+            return warp_lower_bound(a.start, col_cell0 + cr.zb, col_cell0 + cr.ze, target, lane) - col_cell0;
+        };
+        if (a.phi_cells) {
+            zw0 = warp == 0 ? cr.zb : lb(t0);
+            zw1 = warp == NW - 1 ? cr.ze : lb(t1);
+            pw0 = cstart(zw0);
+            pw1 = cstart(zw1);
+        } else {
+            pw0 = t0;
+            pw1 = t1;
+            zw0 = t0 < t1 ? lb(t0 + 1) - 1 : cr.zb;
+            zw1 = t0 < t1 ? lb(t1) : cr.zb;
+        }
     }
-    int s_next = cstart(zw0);
     for (int c2 = zw0; c2 < zw1; ++c2) {
-        const int s0 = s_next, s1 = cstart(c2 + 1);
-        s_next = s1;
-        if (s0 == s1) {
+        const int s0 = max(cstart(c2), pw0), s1 = min(cstart(c2 + 1), pw1);
+        if (s0 >= s1) {
             if (a.phi_cells)
                 for (int node = lane; node < L3; node += 32)
                     a.phi_cells[(int64_t)(col_cell0 + c2) * L3 + node] = 0.0;
@@ -834,12 +846,15 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, in
         double acc[NT][2];
 #pragma unroll
         for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
-        // lanes past the chunk end clamp to a valid particle and carry q = 0
-        double4 nxt = ld_rec(a.sp + s0 + min(p, s1 - s0 - 1));
+        // lanes past the chunk end clamp to a valid particle and carry q = 0;
+        // records of the next two chunks in flight
+        double4 nxt = ld_rec(a.sp + min(s0 + p, s1 - 1));
+        double4 nxt2 = ld_rec(a.sp + min(s0 + 16 + p, s1 - 1));
         for (int base = s0; base < s1; base += 16) {
             const int cnt = min(16, s1 - base);
-            const double4 pt = nxt;  // software prefetch of the next chunk
-            if (base + 16 < s1) nxt = ld_rec(a.sp + base + 16 + min(p, s1 - base - 16 - 1));
+            const double4 pt = nxt;
+            nxt = nxt2;
+            if (base + 32 < s1) nxt2 = ld_rec(a.sp + min(base + 32 + p, s1 - 1));
             const double q = p < cnt ? pt.w : 0.0;
             qsum += h == 0 ? q : 0.0;
             const double t0 = (pt.x - ax0.mid) * ax0.inv;

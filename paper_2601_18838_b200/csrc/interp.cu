@@ -732,14 +732,11 @@ struct UvMap {
     __host__ __device__ static constexpr bool multi(int g) { return NT > 1 && pair(g, 1) >= 0; }
     static constexpr int stage = 16 * 8 * 2 + 16 * 2;  // A rows, U rows, (t1, t2)
     static constexpr int ph = MT2 * 8 * LDK;
-    static constexpr int area = stage > ph ? stage : ph;
+    static constexpr int area = stage + ph;  // ph separate: its padding is zeroed once
 };
 
-// T1 partial row stride: >= the padded R and = 8 mod 16 doubles, so the
-// per-cell double2 accumulate (two rows per 8-lane phase) is conflict-free.
-__host__ __device__ constexpr int uv_t1_stride(int R) {
-    return ((R + 7) / 8) * 8 % 16 == 8 ? ((R + 7) / 8) * 8 : ((R + 7) / 8) * 8 + 8;
-}
+// T1 partial row stride (the padded R; shared memory is the occupancy limit).
+__host__ __device__ constexpr int uv_t1_stride(int R) { return ((R + 7) / 8) * 8; }
 
 template <int L>
 __host__ __device__ constexpr int spread_uv_warp_doubles(int R) {
@@ -779,13 +776,14 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, in
     double* As = sm + warp * per_warp;  // [16][8] swizzled rows q t0^i
     double* Us = As + 16 * 8;           // [16][8] swizzled rows U
     double2* Ts = reinterpret_cast<double2*>(Us + 16 * 8);  // [16] (t1, t2)
-    double* ph = As;                    // [MT2*8][LDK] finished cell grid (aliases staging)
+    double* ph = As + M::stage;         // [MT2*8][LDK] finished cell grid
     double* t1w = As + M::area;         // [MT2*8][RP]  warp partial of T1
     double* w2s = sm + NW * per_warp;   // [R][n2] W2 (monomial rows), shared by the CTA
     double* epi = w2s + R * n2;
     __shared__ double red[128];
     __shared__ int cst[66];             // cell starts of this column segment (+1)
     for (int e = lane; e < MT2 * 8 * RP; e += 32) t1w[e] = 0.0;
+    for (int e = lane; e < M::ph; e += 32) ph[e] = 0.0;  // padding stays zero
     for (int e0 = threadIdx.x; e0 < R * n2; e0 += 128 * 8) {  // loads in flight together
         double v[8];
 #pragma unroll
@@ -805,7 +803,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, in
     const int p = lane & 15, h = lane >> 4;
     const int gg = lane >> 2, tg = lane & 3;
     const bool use_t2 = gg < L, multi = M::multi(gg);
-    unsigned long long badf = 0;
+    double tmax = 0.0;  // largest |t| seen (out-of-cell check at the end)
     double qsum = 0.0;
     __syncthreads();
     auto cstart = [&](int c2) { return cst_ok ? cst[c2 - cr.zb] : a.start[col_cell0 + c2]; };
@@ -860,8 +858,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, in
             const double t0 = (pt.x - ax0.mid) * ax0.inv;
             const double t1 = (pt.y - ax1.mid) * ax1.inv;
             const double t2 = (pt.z - ax2.mid) * ax2.inv;
-            // tensor_weights' out-of-cell check, |t| <= 1 + 2e-12 (slack 1e-12 of the width)
-            badf |= fmax(fabs(t0), fmax(fabs(t1), fabs(t2))) > 1.0 + 2e-12 ? 1ull : 0ull;
+            tmax = fmax(tmax, fmax(fabs(t0), fmax(fabs(t1), fabs(t2))));
             __syncwarp();  // previous chunk's fragment reads done
             double row[8];
             if (h == 0) {
@@ -906,15 +903,13 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, in
                 for (int t = 0; t < NT; ++t) dmma884(acc[t], af, v[t]);
             }
         }
-        __syncwarp();  // staging reads done: reuse it as ph[(i,j)][k]
+        __syncwarp();
         if (UV_SKIP & 8) {  // ablation: raw fragments straight to global
             double2* o = reinterpret_cast<double2*>(uv_scratch) + ((int64_t)(col_cell0 + c2) * NT) * 32 + lane;
 #pragma unroll
             for (int t = 0; t < NT; ++t) o[t * 32] = make_double2(acc[t][0], acc[t][1]);
         }
         if (UV_SKIP & 2) continue;
-        for (int e = lane; e < MT2 * 8 * LDK; e += 32) ph[e] = 0.0;
-        __syncwarp();
         const int i_row = lane >> 2;
         if (i_row < L) {
 #pragma unroll
@@ -964,8 +959,9 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, in
         }
         __syncwarp();
     }
-    badf = __reduce_or_sync(0xffffffffu, (unsigned)badf);
-    if (lane == 0 && badf) atomicOr(&a.bad[1], 1ull);
+    // tensor_weights' out-of-cell check, |t| <= 1 + 2e-12 (slack 1e-12 of the width)
+    const unsigned badw = __ballot_sync(0xffffffffu, !(tmax <= 1.0 + 2e-12));
+    if (lane == 0 && badw) atomicOr(&a.bad[1], 1ull);
     if (UV_SKIP & 4) return;
     spread_epilogue<L>(a, cr, sm, per_warp, M::area, RP, epi, red, qsum, want_fwd);
 }

@@ -1,0 +1,16 @@
+#!/bin/bash
+# On the GPU box: default bench line, the ncu launch list of a short bench
+# run, and one ncu --set full capture of the pipeline (config 3). Outputs in
+# gpurun_out/; copy the summaries into profiles/ afterwards.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err || { tail -20 gpurun_out/bench.err; exit 1; }
+cat gpurun_out/bench.json
+python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > /dev/null 2>&1 || exit 1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/ncu_launch.log 2>&1
+python scripts/profile_step.py cfg3 2 > /dev/null 2>&1 || exit 1
+ncu --set full --clock-control none --import-source on \
+    -k regex:"k_spread|k_bwd_gather|k_col_scatter|k_z_sort|k_tile_hist|k_col_scan|k_core_sum" -c 7 \
+    -f -o gpurun_out/full python scripts/profile_step.py cfg3 1 > gpurun_out/ncu_full.log 2>&1
+tail -1 gpurun_out/ncu_full.log

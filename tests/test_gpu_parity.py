@@ -377,3 +377,40 @@ def test_dgemm_tn(M, N, K):
     assert float(torch.linalg.norm(out - ref) / torch.linalg.norm(ref)) <= 1e-14
     dgemm_tn(a, f, out, accumulate=True)
     assert float(torch.linalg.norm(out - 2 * ref) / torch.linalg.norm(ref)) <= 1e-14
+
+
+# ---- every order of the monomial hot path (L <= 8) and both psi paths -------
+
+@pytest.mark.parametrize("order,modes,counts", [
+    (2, 3, (3, 4, 5)), (3, 3, (4, 3, 2)), (4, 2, (5, 5, 5)), (5, 4, (3, 3, 7)),
+    (6, 5, (4, 4, 4)), (7, 3, (2, 3, 4)), (8, 4, (3, 2, 3)),
+    (6, 8, (3, 3, 3)),   # R = 17: the scalar psi contraction of the gather
+    (4, 1, (6, 6, 6)),   # R = 3
+])
+def test_e2e_orders_vs_oracle(oracle, order, modes, counts):
+    """The factored-operand spread (UvMap column maps differ per L) and the
+    gather for every L <= 8, against the oracle at 1e-10."""
+    from oracle.binding import make_problem
+
+    pb = make_problem(oracle, n=1500, counts=counts, order=order, modes=modes, eps=1e-8,
+                      seed=order * 10 + modes, charges="neutral")
+    plan = plan_for(pb)
+    z = plan.execute(dev(pb.pos), dev(pb.q)).cpu().numpy()
+    assert rel(z, oracle.kpme_apply(pb)) <= E2E_TOL
+
+
+@pytest.mark.parametrize("order", [4, 6, 8])
+def test_e2e_clustered_cells(oracle, order):
+    """Most particles in a few cells: long chunk streams inside one cell, warps
+    sharing cells, columns above the whole-column sort capacity."""
+    from oracle.binding import make_problem
+
+    pb = make_problem(oracle, n=20000, counts=(4, 4, 4), order=order, modes=3, eps=1e-8, seed=7)
+    pos = np.array(pb.pos)
+    rng = np.random.default_rng(order)
+    # 15000 inside the 2x2x2 central cells: ~3750 per central column (> 2560)
+    pos[:15000] = 0.5 + 0.1 * (rng.random((15000, 3)) - 0.5)
+    pb.pos = pos
+    plan = plan_for(pb)
+    z = plan.execute(dev(pb.pos), dev(pb.q)).cpu().numpy()
+    assert rel(z, oracle.kpme_apply(pb)) <= E2E_TOL

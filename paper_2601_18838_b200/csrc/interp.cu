@@ -972,8 +972,15 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, in
 // scattered straight to global particle order.
 constexpr int GT = 128;  // gather threads per CTA
 
+constexpr int kGatherTab = 32;  // batch cells with shared-memory start/axis tables
 template <int L, int MODE, bool MONO>
-__global__ void __launch_bounds__(GT, 512 / GT) k_bwd_gather_t(ColumnArgs a, int cells_per_batch) {
+#ifndef GATHER_SKIP
+#define GATHER_SKIP 0  // profiling ablations only: 1 particle loop, 2 Horner
+#endif
+#ifndef GATHER_MINB
+#define GATHER_MINB (512 / GT)
+#endif
+__global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, int cells_per_batch) {
     constexpr int L2 = L * L, L3 = L2 * L;
     const Geometry& g = a.g;
     const int R = g.R, tid = threadIdx.x;
@@ -982,6 +989,8 @@ __global__ void __launch_bounds__(GT, 512 / GT) k_bwd_gather_t(ColumnArgs a, int
     double* b2s = sm;             // L^2 x R
     double* psi = b2s + L2 * R;   // cells_per_batch x L^3
     __shared__ double lc[16];
+    __shared__ int gcst[kGatherTab + 1];
+    __shared__ double4 gax[kGatherTab];
     lagrange_consts(L, lc);
     double corr = a.corr ? *a.corr : 0.0;
     if (MODE != GATHER_FROM_CELLS && a.B2 == nullptr) {
@@ -1085,7 +1094,59 @@ __global__ void __launch_bounds__(GT, 512 / GT) k_bwd_gather_t(ColumnArgs a, int
             }
         }
         __syncthreads();
-        if (MODE != PSI_ONLY) {
+        if (MONO && MODE != PSI_ONLY && !(GATHER_SKIP & 1) && cb1 - cb0 <= kGatherTab) {
+            // cell starts and z axes of the batch in shared memory; each thread
+            // walks its particles in increasing order, so its cell only advances
+            const int nb = cb1 - cb0;
+            for (int e = tid; e <= nb; e += GT) gcst[e] = a.start[cell0 + e];
+            for (int e = tid; e < nb; e += GT) gax[e] = a.cellax[2][cb0 + e];
+            __syncthreads();
+            const int s0 = gcst[0], s1 = gcst[nb];
+            int cc = 0;
+            double tmax = 0.0;
+            double4 pn = s0 + tid < s1 ? ld_rec(a.sp + s0 + tid) : make_double4(0.0, 0.0, 0.0, 0.0);
+            int dn = s0 + tid < s1 ? a.perm[s0 + tid] : 0;
+            for (int s = s0 + tid; s < s1; s += GT) {
+                const double4 p = pn;  // software prefetch of the next particle
+                const int dst = dn;
+                if (s + GT < s1) {
+                    pn = ld_rec(a.sp + s + GT);
+                    dn = a.perm[s + GT];
+                }
+                while (gcst[cc + 1] <= s) ++cc;
+                const double* ps = psi + cc * L3;
+                const double4 x2 = gax[cc];  // (lo, hi, mid, inv)
+                double t[3];
+                t[0] = (p.x - ax0.mid) * ax0.inv;
+                t[1] = (p.y - ax1.mid) * ax1.inv;
+                t[2] = (p.z - x2.z) * x2.w;
+                tmax = fmax(tmax, fmax(fabs(t[0]), fmax(fabs(t[1]), fabs(t[2]))));
+                double z = 0.0;
+                if (GATHER_SKIP & 2) {
+                    z = t[0] + t[1] + t[2] + ps[0];
+                } else {
+                    // ps = monomial coefficients C[a][b][c] of this cell's potential:
+                    // z = sum_a t0^a sum_b t1^b sum_c t2^c C[a][b][c] (nested Horner)
+#pragma unroll
+                    for (int i = L - 1; i >= 0; --i) {
+                        double zb = 0.0;
+#pragma unroll
+                        for (int j = L - 1; j >= 0; --j) {
+                            const double* row = ps + (i * L + j) * L;
+                            double zc = row[L - 1];
+#pragma unroll
+                            for (int k = L - 2; k >= 0; --k) zc = fma(zc, t[2], row[k]);
+                            zb = fma(zb, t[1], zc);
+                        }
+                        z = fma(z, t[0], zb);
+                    }
+                }
+                a.out[dst] = z - corr;
+            }
+            // tensor_weights' out-of-cell check, |t| <= 1 + 2e-12 (slack 1e-12 of the width)
+            if (__ballot_sync(0xffffffffu, !(tmax <= 1.0 + 2e-12)) && (tid & 31) == 0)
+                atomicOr(&a.bad[1], 1ull);
+        } else if (MODE != PSI_ONLY && !(GATHER_SKIP & 1)) {
             const int s0 = a.start[cell0], s1 = a.start[cell0 + (cb1 - cb0)];
             double4 pn = s0 + tid < s1 ? ld_rec(a.sp + s0 + tid) : make_double4(0.0, 0.0, 0.0, 0.0);
             int dn = s0 + tid < s1 ? a.perm[s0 + tid] : 0;
@@ -1100,7 +1161,9 @@ __global__ void __launch_bounds__(GT, 512 / GT) k_bwd_gather_t(ColumnArgs a, int
                 const double* ps = psi + (c2 - cb0) * L3;
                 const CellAxis ax2 = cell_axis_tab(a.cellax[2], c2);
                 double z = 0.0;
-                if (MONO) {
+                if (GATHER_SKIP & 2) {
+                    z = p.x + p.y + p.z + ps[0];
+                } else if (MONO) {
                     // ps = monomial coefficients C[a][b][c] of this cell's potential:
                     // z = sum_a t0^a sum_b t1^b sum_c t2^c C[a][b][c] (nested Horner)
                     double t[3];
@@ -1235,9 +1298,17 @@ void launch_gather_mode(const ColumnArgs& a, int grid, int cb, size_t smem, cuda
 }
 
 template <int L>
-void launch_gather_t(const ColumnArgs& a, int mode, cudaStream_t s) {
+void launch_gather_t(const ColumnArgs& a0, int mode, cudaStream_t s) {
+    ColumnArgs a = a0;
+#ifdef GATHER_S
+    if (mode == GATHER_FROM_B2 && a.B2 == nullptr) a.S = std::max(1, std::min(GATHER_S, a.g.z_hi - a.g.z_lo));
+#endif
     const int grid = a.g.K[0] * a.g.K[1] * a.S;
+#ifdef GATHER_CB
+    const int cb = std::min(gather_batch(a.g), GATHER_CB);
+#else
     const int cb = gather_batch(a.g);
+#endif
     const int R = a.g.R;
     const size_t smem = sizeof(double) * ((size_t)L * L * R + (size_t)cb * L * L * L +
                                           (size_t)R * R * R + (size_t)L * R * R +

@@ -1000,7 +1000,18 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
         double* h = psi + (size_t)cells_per_batch * L3;  // [R^3]  G .* F
         double* v = h + RR * R;                          // [L][R][R]
         double* w01 = v + L * RR;                        // [2][R][L] W0, W1 column rows
-        for (int e = tid; e < RR * R; e += GT) h[e] = a.Gc[e] * a.Fc[e];
+        for (int e0 = tid; e0 < RR * R; e0 += GT * 8) {  // loads in flight together
+            double gv[8], fv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (e0 + GT * u < RR * R) {
+                    gv[u] = __ldg(a.Gc + e0 + GT * u);
+                    fv[u] = __ldg(a.Fc + e0 + GT * u);
+                }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (e0 + GT * u < RR * R) h[e0 + GT * u] = gv[u] * fv[u];
+        }
         for (int e = tid; e < R * L; e += GT) {
             w01[e] = a.W0[(int64_t)(e / L) * g.n[0] + cr.c0 * L + e % L];
             w01[R * L + e] = a.W1[(int64_t)(e / L) * g.n[1] + cr.c1 * L + e % L];
@@ -1035,8 +1046,17 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
         const int cell0 = (cr.c0 * g.K[1] + cr.c1) * g.K[2] + cb0;
         const int nz = (cb1 - cb0) * L;
         if (MODE != GATHER_FROM_CELLS) {
-            for (int e = tid; e < R * nz; e += GT)
-                w2s[e] = a.W2[(int64_t)(e / nz) * g.n[2] + cb0 * L + e % nz];
+            for (int e0 = tid; e0 < R * nz; e0 += GT * 8) {  // loads in flight together
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = e0 + GT * u;
+                    if (e < R * nz) v[u] = __ldg(a.W2 + (int64_t)(e / nz) * g.n[2] + cb0 * L + e % nz);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (e0 + GT * u < R * nz) w2s[e0 + GT * u] = v[u];
+            }
             __syncthreads();
         }
         if (MODE == GATHER_FROM_CELLS) {

@@ -126,9 +126,15 @@ int kpme_gpu_plan_destroy(kpme_gpu_plan plan);
  * the legacy default stream, which cannot be graph-captured). A new plan
  * owns a non-blocking stream. */
 int kpme_gpu_plan_set_stream(kpme_gpu_plan plan, void* stream);
-/* Host buffers; H2D of xyz/q and D2H of potentials happen inside. */
+/* Host buffers; H2D of xyz/q and D2H of potentials happen inside. Large
+ * calls are pipelined in particle chunks: each chunk is sorted and spread
+ * while the next one crosses PCIe, and the potentials leave chunk by chunk
+ * behind the gather. Pinned host buffers give full overlap. */
 int kpme_gpu_plan_execute(kpme_gpu_plan plan, int64_t n, const double* xyz,
                           const double* q, double* potentials);
+/* Chunk count of kpme_gpu_plan_execute: -1 automatic (one chunk per ~256K
+ * particles, at most 8), 1 = unpipelined, else 2..8. */
+int kpme_gpu_plan_set_host_chunks(kpme_gpu_plan plan, int chunks);
 /* Device buffers, stream-ordered. flags & KPME_GPU_DEFER_CHECKS skips the
  * stream synchronisation that reports invalid particles; call
  * kpme_gpu_plan_status() later instead. */

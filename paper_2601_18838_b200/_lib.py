@@ -76,6 +76,7 @@ def _load():
         "kpme_gpu_plan_destroy": (C.c_int, [P]),
         "kpme_gpu_plan_set_stream": (C.c_int, [P, P]),
         "kpme_gpu_plan_execute": (C.c_int, [P, C.c_int64, _dp, _dp, _dp]),
+        "kpme_gpu_plan_set_host_chunks": (C.c_int, [P, C.c_int]),
         "kpme_gpu_plan_execute_device": (C.c_int, [P, C.c_int64, P, P, P, C.c_int]),
         "kpme_gpu_plan_status": (C.c_int, [P]),
         "kpme_gpu_plan_launches": (C.c_int, [P]),
@@ -119,6 +120,7 @@ EXPORTS = sorted(
         "kpme_gpu_dense_workspace_bytes", "kpme_gpu_kron_matvec_dense",
         "kpme_gpu_plan_axis_operands", "kpme_gpu_dgemm_tn", "kpme_gpu_plan_create_slab",
         "kpme_gpu_plan_core_size", "kpme_gpu_plan_forward", "kpme_gpu_plan_backward",
+        "kpme_gpu_plan_set_host_chunks",
     ]
 )
 

@@ -200,6 +200,9 @@ __global__ void k_factor_wl(Geometry g, int a, const double* __restrict__ W,
         const int r = e / n, x = e % n, c = x / L, m = x % L;
         double s = 0.0;
         for (int i = 0; i < L; ++i) s = fma(W[(int64_t)r * n + c * L + i], lam[i * L + m], s);
+        // r = 0 is the constant row: sum_i w_i(t) = 1 exactly (interpolation
+        // reproduces constants), so its monomial row is exactly (1, 0, ..., 0)
+        if (r == 0) s = m == 0 ? 1.0 : 0.0;
         WL[e] = s;
     }
 }

@@ -111,7 +111,8 @@ struct ColumnArgs {
     // rebuilds its B2 block from the summed core
     const double* W0;        // [R][n0]
     const double* W1;        // [R][n1]
-    double* Fpart;           // [S*K0*K1][R^3+1] partial cores (last entry: sum q)
+    double* Fpart;           // [R^3+1][fstride] partial cores (last entry: sum q)
+    int fstride;             // Fpart row stride; 0 = S*K0*K1 (one particle chunk)
     const double* Gc;        // [R^3] collapsed SKP core
     const double* Fc;        // [R^3+1] summed core
     double correction;       // c_Lambda

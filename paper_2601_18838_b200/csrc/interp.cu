@@ -487,7 +487,7 @@ __device__ __forceinline__ void spread_epilogue(const ColumnArgs& a, const Colum
         }
         __syncthreads();
         // Fpart is entry-major, [R^3+1][nblocks], so k_core_sum reads it coalesced
-        const int nblocks = a.S * g.K[0] * g.K[1];
+        const int nblocks = a.fstride > 0 ? a.fstride : a.S * g.K[0] * g.K[1];
         double* dst = a.Fpart + (int64_t)cr.seg * g.K[0] * g.K[1] + cr.col;
         for (int e = threadIdx.x; e < R * R * R; e += 128) {
             const int r0 = e / (R * R), rr = e % (R * R);
@@ -1012,6 +1012,15 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
             for (int u = 0; u < 8; ++u)
                 if (e0 + GT * u < RR * R) h[e0 + GT * u] = gv[u] * fv[u];
         }
+        if (MONO && tid == 0) {
+            // Zero mode, exactly: the m = 0 rows of W_a are the constant 1 and
+            // Lagrange interpolation reproduces constants, so F[0,0,0] = sum q
+            // and (W^T (G .* F))[0] - c sum q = (G[0] - c) sum q. Evaluated
+            // this way, not as the difference of two rounded sums over all
+            // particles, which for a neutral system leaves a uniform offset
+            // of pure rounding noise ("zero mode").
+            h[0] = (__ldg(a.Gc) - a.correction) * __ldg(a.Fc + RR * R);
+        }
         for (int e = tid; e < R * L; e += GT) {
             w01[e] = a.W0[(int64_t)(e / L) * g.n[0] + cr.c0 * L + e % L];
             w01[R * L + e] = a.W1[(int64_t)(e / L) * g.n[1] + cr.c1 * L + e % L];
@@ -1030,7 +1039,7 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
             for (int r1 = 0; r1 < R; ++r1) s = fma(w01[R * L + r1 * L + j], v[i * RR + r1 * R + r2], s);
             b2s[e] = s;
         }
-        corr = a.correction * a.Fc[RR * R];
+        corr = MONO ? 0.0 : a.correction * a.Fc[RR * R];
     } else if (MODE != GATHER_FROM_CELLS) {
         for (int e = tid; e < L2 * R; e += GT) {
             const int ij = e / R, r = e % R, i = ij / L, j = ij % L;

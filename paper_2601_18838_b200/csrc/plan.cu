@@ -23,6 +23,9 @@ extern thread_local std::string g_last_error;
 
 using kb::Error;
 
+// Particle chunks of the pipelined host path (kpme_gpu_plan_execute).
+constexpr int kMaxChunks = 8;
+
 struct kpme_gpu_plan_s {
     kb::Geometry g{};
     int device = 0;
@@ -62,6 +65,15 @@ struct kpme_gpu_plan_s {
     double* q_d = nullptr;
     double* out_d = nullptr;
     unsigned long long* flags_h = nullptr;  // pinned
+    // chunked host path (kpme_gpu_plan_execute): copies on their own stream,
+    // one independent sort + spread per particle chunk
+    int host_chunks = -1;                   // -1: automatic
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_in[kMaxChunks] = {}, ev_out[kMaxChunks] = {};
+    int32_t* cstart = nullptr;              // [kMaxChunks][ncell + 1]
+    unsigned long long* cbad = nullptr;     // [kMaxChunks][2]
+    unsigned long long* cflags_h = nullptr; // pinned [kMaxChunks][2]
+    double* cFpart = nullptr;               // [R^3 + 1][kMaxChunks * S * ncol]
     // dense form
     double* A[3] = {nullptr, nullptr, nullptr};
     double* cells = nullptr;
@@ -89,6 +101,12 @@ struct kpme_gpu_plan_s {
     ~kpme_gpu_plan_s() {
         cudaSetDevice(device);
         if (gexec) cudaGraphExecDestroy(gexec);
+        for (int c = 0; c < kMaxChunks; ++c) {
+            if (ev_in[c]) cudaEventDestroy(ev_in[c]);
+            if (ev_out[c]) cudaEventDestroy(ev_out[c]);
+        }
+        if (cstream) cudaStreamDestroy(cstream);
+        if (cflags_h) cudaFreeHost(cflags_h);
         for (auto e : ev) cudaEventDestroy(e);
         for (void* p : allocs) cudaFree(p);
         if (flags_h) cudaFreeHost(flags_h);
@@ -275,6 +293,135 @@ void backward_half(kpme_gpu_plan p, const double* core, double* out) {
     if (p->g.L <= 8) mono_tables(p, a);
     kb::launch_bwd_gather(a, kb::GATHER_FROM_B2, p->stream);
     p->launches += 1;
+}
+
+// ---- pipelined host path ------------------------------------------------------
+//
+// kpme_gpu_plan_execute on host buffers. The collapsed operator is linear in
+// the particles, so the particle set is cut into C contiguous chunks, each
+// sorted and spread on its own into per-column partial cores while the next
+// chunk is still crossing PCIe; after the last chunk the partial cores of all
+// chunks are summed in a fixed order and the gather runs chunk by chunk, each
+// chunk's potentials leaving for the host while the next one is computed.
+// The result is deterministic for a given (n, C) and within rounding of the
+// unchunked pipeline (the partial cores are summed in another order).
+
+int chunk_count(kpme_gpu_plan p, int64_t n) {
+    if (p->form == KPME_GPU_FORM_DENSE || p->g.L > 8) return 1;
+    int c = p->host_chunks;
+    if (c < 0) c = (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, (n + 131072) / 262144));
+    return std::max(1, std::min(c, kMaxChunks));
+}
+
+void ensure_host_buffers(kpme_gpu_plan p, bool chunked) {
+    if (!p->xyz_d) {
+        p->xyz_d = p->alloc<double>((size_t)p->cap * 3);
+        p->q_d = p->alloc<double>(p->cap);
+        p->out_d = p->alloc<double>(p->cap);
+    }
+    if (!chunked || p->cstream) return;
+    const kb::Geometry& g = p->g;
+    const size_t nb = (size_t)p->S * g.K[0] * g.K[1];
+    p->cstart = p->alloc<int32_t>((size_t)kMaxChunks * (g.ncell + 1));
+    p->cbad = p->alloc<unsigned long long>(2 * kMaxChunks);
+    p->cFpart = p->alloc<double>((size_t)kMaxChunks * nb * ((size_t)g.R * g.R * g.R + 1));
+    // [0, 2C): flags read back; [2C, 4C): the reset pattern (ULLONG_MAX, 0)
+    KB_CUDA(cudaMallocHost(&p->cflags_h, 4 * kMaxChunks * sizeof(unsigned long long)));
+    for (int c = 0; c < kMaxChunks; ++c) {
+        p->cflags_h[2 * kMaxChunks + 2 * c] = ULLONG_MAX;
+        p->cflags_h[2 * kMaxChunks + 2 * c + 1] = 0ull;
+        KB_CUDA(cudaEventCreateWithFlags(&p->ev_in[c], cudaEventDisableTiming));
+        KB_CUDA(cudaEventCreateWithFlags(&p->ev_out[c], cudaEventDisableTiming));
+    }
+    KB_CUDA(cudaStreamCreateWithFlags(&p->cstream, cudaStreamNonBlocking));
+}
+
+void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q, double* out,
+                     int C) {
+    const kb::Geometry& g = p->g;
+    // chunk boundaries on 2048-particle tiles keep every per-chunk slice as
+    // aligned as the buffers' bases
+    const int64_t step = ((n + C - 1) / C + 2047) / 2048 * 2048;
+    C = (int)((n + step - 1) / step);
+    const int nb = p->S * g.K[0] * g.K[1];
+    p->launches = 0;
+    // the copy stream starts after the work already queued on the plan stream
+    KB_CUDA(cudaEventRecord(p->ev_out[kMaxChunks - 1], p->stream));
+    KB_CUDA(cudaStreamWaitEvent(p->cstream, p->ev_out[kMaxChunks - 1], 0));
+    for (int c = 0; c < C; ++c) {
+        const int64_t off = c * step, nc = std::min(step, n - off);
+        KB_CUDA(cudaMemcpyAsync(p->xyz_d + 3 * off, xyz + 3 * off, sizeof(double) * 3 * nc,
+                                cudaMemcpyHostToDevice, p->cstream));
+        KB_CUDA(cudaMemcpyAsync(p->q_d + off, q + off, sizeof(double) * nc,
+                                cudaMemcpyHostToDevice, p->cstream));
+        KB_CUDA(cudaEventRecord(p->ev_in[c], p->cstream));
+    }
+    KB_CUDA(cudaMemcpyAsync(p->cbad, p->cflags_h + 2 * kMaxChunks,
+                            2 * C * sizeof(unsigned long long), cudaMemcpyHostToDevice, p->stream));
+    auto chunk_args = [&](int c, kb::SortBuffers& sb) {
+        const int64_t off = c * step;
+        sb = p->sb;
+        sb.start = p->cstart + (size_t)c * (g.ncell + 1);
+        sb.perm = p->sb.perm + off;
+        sb.bad = p->cbad + 2 * c;
+        kb::ColumnArgs a = column_args(p);
+        a.start = sb.start;
+        a.sp = p->sp + off;
+        a.perm = sb.perm;
+        a.bad = sb.bad;
+        mono_tables(p, a);
+        return a;
+    };
+    // forward: per chunk sort + spread into its block of partial cores
+    for (int c = 0; c < C; ++c) {
+        const int64_t off = c * step, nc = std::min(step, n - off);
+        KB_CUDA(cudaStreamWaitEvent(p->stream, p->ev_in[c], 0));
+        kb::SortBuffers sb;
+        kb::ColumnArgs a = chunk_args(c, sb);
+        if (p->use_sort2)
+            kb::launch_sort2(g, nc, p->xyz_d + 3 * off, sb, p->stream, &p->launches, p->q_d + off,
+                             p->sp + off);
+        else
+            kb::launch_sort(g, nc, p->xyz_d + 3 * off, sb, p->stream, &p->launches, p->q_d + off,
+                            p->sp + off);
+        a.Fpart = p->cFpart + (size_t)c * nb;
+        a.fstride = C * nb;
+        kb::launch_spread_fwd(a, kb::SPREAD_PARTICLES, true, p->stream);
+        ++p->launches;
+    }
+    kb::launch_core_sum(g, C * nb, p->cFpart, p->F, p->stream);
+    ++p->launches;
+    // backward + gather per chunk; its potentials leave while the next runs
+    for (int c = 0; c < C; ++c) {
+        const int64_t off = c * step, nc = std::min(step, n - off);
+        kb::SortBuffers sb;
+        kb::ColumnArgs a = chunk_args(c, sb);
+        a.out = p->out_d + off;
+        a.B2 = nullptr;
+        a.Fc = p->F;
+        a.corr = nullptr;
+        kb::launch_bwd_gather(a, kb::GATHER_FROM_B2, p->stream);
+        ++p->launches;
+        KB_CUDA(cudaEventRecord(p->ev_out[c], p->stream));
+        KB_CUDA(cudaStreamWaitEvent(p->cstream, p->ev_out[c], 0));
+        KB_CUDA(cudaMemcpyAsync(out + off, p->out_d + off, sizeof(double) * nc,
+                                cudaMemcpyDeviceToHost, p->cstream));
+    }
+    KB_CUDA(cudaMemcpyAsync(p->cflags_h, p->cbad, 2 * C * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, p->cstream));
+    KB_CUDA(cudaStreamSynchronize(p->cstream));
+    // the reference reports the first particle outside the box
+    // (assign_particles, geometry.hpp:136-138) before any cell check
+    for (int c = 0; c < C; ++c)
+        if (p->cflags_h[2 * c] != ULLONG_MAX)
+            throw Error(KPME_GPU_INVALID_ARGUMENT,
+                        "assign_particles: particle " +
+                            std::to_string(c * step + (int64_t)p->cflags_h[2 * c]) +
+                            " outside the box");
+    unsigned long long any = 0;
+    for (int c = 0; c < C; ++c) any |= p->cflags_h[2 * c + 1];
+    const unsigned long long f[2] = {ULLONG_MAX, any};
+    check_flags(f);
 }
 
 void collect_times(kpme_gpu_plan p) {
@@ -532,10 +679,11 @@ extern "C" int kpme_gpu_plan_execute(kpme_gpu_plan p, int64_t n, const double* x
         if (!p) invalid("kpme_gpu: null plan");
         if (n > p->cap) invalid("kpme_gpu: more particles than the plan was created for");
         KB_CUDA(cudaSetDevice(p->device));
-        if (!p->xyz_d) {
-            p->xyz_d = p->alloc<double>((size_t)p->cap * 3);
-            p->q_d = p->alloc<double>(p->cap);
-            p->out_d = p->alloc<double>(p->cap);
+        const int C = chunk_count(p, n);
+        ensure_host_buffers(p, C > 1);
+        if (C > 1 && !p->timing) {
+            execute_chunked(p, n, xyz, q, out, C);
+            return;
         }
         if (n > 0) {
             KB_CUDA(cudaMemcpyAsync(p->xyz_d, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice,
@@ -549,6 +697,14 @@ extern "C" int kpme_gpu_plan_execute(kpme_gpu_plan p, int64_t n, const double* x
                                     p->stream));
         sync_and_check(p);
         collect_times(p);
+    });
+}
+
+extern "C" int kpme_gpu_plan_set_host_chunks(kpme_gpu_plan p, int chunks) {
+    return guarded([&] {
+        if (!p) invalid("kpme_gpu: null plan");
+        if (chunks > kMaxChunks) invalid("kpme_gpu_plan_set_host_chunks: more than 8 chunks");
+        p->host_chunks = chunks < 0 ? -1 : std::max(1, chunks);
     });
 }
 

@@ -116,6 +116,10 @@ class KpmePlan:
                                         out.ctypes.data_as(dp)))
         return out[:n]
 
+    def set_host_chunks(self, chunks: int):
+        """Particle chunks of the pipelined host path (-1 automatic, 1 off)."""
+        check(lib.kpme_gpu_plan_set_host_chunks(self._h, int(chunks)))
+
     def execute_host_ptr(self, n: int, xyz_ptr: int, q_ptr: int, out_ptr: int):
         """Host-pointer variant for pinned torch CPU tensors."""
         dp = C.POINTER(C.c_double)

@@ -269,6 +269,65 @@ def test_e2e_cfg3_vs_oracle(oracle):
                  q=w.data.charges.values)
     ref = oracle.kpme_apply(pb, fuse_terms=False, threads=os.cpu_count() or 1)
     assert rel(z, ref) <= E2E_TOL
+    # the pipelined host path (automatic chunking: 4 chunks at 10^6 particles)
+    zh = plan.execute_host(w.data.cloud.positions, w.data.charges.values)
+    assert rel(zh, ref) <= E2E_TOL
+    assert rel(zh, z) <= 1e-13
+    assert np.array_equal(zh, plan.execute_host(w.data.cloud.positions, w.data.charges.values))
+
+
+@pytest.mark.parametrize("chunks", [1, 2, 3, 8])
+def test_host_path_chunks(oracle, chunks):
+    """kpme_gpu_plan_execute pipelined over particle chunks (each chunk sorted
+    and spread on its own, partial cores summed in chunk order) against the
+    oracle, the unchunked device path, and the reference's error contract:
+    the first particle outside the box is reported by its global index."""
+    from oracle.binding import make_problem
+
+    pb = make_problem(oracle, n=30000, counts=(5, 6, 7), order=6, modes=4, eps=1e-10, seed=11,
+                      charges="neutral")
+    plan = plan_for(pb)
+    plan.set_host_chunks(chunks)
+    zd = plan.execute(dev(pb.pos), dev(pb.q)).cpu().numpy()
+    zh = plan.execute_host(pb.pos, pb.q)
+    assert rel(zh, oracle.kpme_apply(pb)) <= E2E_TOL
+    assert rel(zh, zd) <= 1e-13
+    bad = np.array(pb.pos)
+    bad[25000] = (1.5, 0.5, 0.5)
+    bad[27000] = (0.5, -0.5, 0.5)
+    with pytest.raises(ValueError, match="particle 25000 outside the box"):
+        plan.execute_host(bad, pb.q)
+    zh2 = plan.execute_host(pb.pos, pb.q)  # the plan recovers after an error
+    assert np.array_equal(zh, zh2)
+
+
+@pytest.mark.parametrize("molecules,K", [(30000, 13), (300000, 29)])
+def test_e2e_water_vs_oracle(oracle, molecules, K):
+    """Config 4's water recipe at 9e4 and 9e5 sites (config 4 itself needs
+    ~25 GB in the reference layout): device path and pipelined host path
+    against the oracle at 1e-10. Neutral molecules make the zero mode a
+    difference of two rounded sums in the reference; the GPU evaluates it
+    exactly, so the residual is the oracle's own rounding."""
+    from oracle.binding import Problem
+    from paper_2601_18838_b200 import inputs
+    import paper_2601_18838_b200 as kp
+    from paper_2601_18838_b200.plan import KpmePlan
+
+    data = inputs.water_cloud(molecules, 0)
+    dec = inputs.decomposition(1e-10)
+    tw, prof = dec.arrays()
+    pb = Problem(xi=3.0, modes=4, center=(0.5, 0.5, 0.5), radius=0.5, counts=(K, K, K), order=6,
+                 term_weights=tw, profiles=prof, correction=dec.correction,
+                 pos=data.cloud.positions, q=data.charges.values)
+    ref = oracle.kpme_apply(pb, threads=os.cpu_count() or 1)
+    grid = kp.build_cell_grid(kp.Box3((0.5, 0.5, 0.5), 0.5), (K, K, K))
+    plan = KpmePlan(kp.EwaldConfig(3.0, 4), grid, 6, dec, len(ref))
+    zd = plan.execute(dev(data.cloud.positions), dev(data.charges.values)).cpu().numpy()
+    assert rel(zd, ref) <= E2E_TOL
+    plan.set_host_chunks(3)
+    zh = plan.execute_host(data.cloud.positions, data.charges.values)
+    assert rel(zh, ref) <= E2E_TOL
+    assert rel(zh, zd) <= 1e-13
 
 
 def test_e2e_cfg4_properties():

@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -309,7 +311,9 @@ void backward_half(kpme_gpu_plan p, const double* core, double* out) {
 int chunk_count(kpme_gpu_plan p, int64_t n) {
     if (p->form == KPME_GPU_FORM_DENSE || p->g.L > 8) return 1;
     int c = p->host_chunks;
-    if (c < 0) c = (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, (n + 131072) / 262144));
+    // automatic: ~1/3 M particles per chunk, at most 4 (measured on B200 at
+    // configs 3 and 4: more chunks add fixed per-chunk sort/spread cost)
+    if (c < 0) c = (int)std::min<int64_t>(4, std::max<int64_t>(1, (n + 166667) / 333333));
     return std::max(1, std::min(c, kMaxChunks));
 }
 
@@ -336,9 +340,39 @@ void ensure_host_buffers(kpme_gpu_plan p, bool chunked) {
     KB_CUDA(cudaStreamCreateWithFlags(&p->cstream, cudaStreamNonBlocking));
 }
 
+// KPME_GPU_TRACE=1: per-chunk timeline of the pipelined host path on stderr
+// (events on both streams, offsets from the first copy; diagnostics only).
+struct ChunkTrace {
+    bool on = false;
+    std::vector<std::pair<std::string, cudaEvent_t>> ev;
+    ChunkTrace() {
+        const char* e = getenv("KPME_GPU_TRACE");
+        on = e && *e && *e != '0';
+    }
+    void mark(const std::string& tag, cudaStream_t s) {
+        if (!on) return;
+        cudaEvent_t e;
+        KB_CUDA(cudaEventCreate(&e));
+        KB_CUDA(cudaEventRecord(e, s));
+        ev.emplace_back(tag, e);
+    }
+    ~ChunkTrace() {
+        if (!on || ev.empty()) return;
+        cudaEventSynchronize(ev.back().second);
+        for (auto& t : ev) {
+            float ms = 0.f;
+            cudaEventSynchronize(t.second);
+            cudaEventElapsedTime(&ms, ev.front().second, t.second);
+            fprintf(stderr, "  %8.1f us  %s\n", ms * 1e3, t.first.c_str());
+        }
+        for (auto& t : ev) cudaEventDestroy(t.second);
+    }
+};
+
 void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q, double* out,
                      int C) {
     const kb::Geometry& g = p->g;
+    ChunkTrace tr;
     // chunk boundaries on 2048-particle tiles keep every per-chunk slice as
     // aligned as the buffers' bases
     const int64_t step = ((n + C - 1) / C + 2047) / 2048 * 2048;
@@ -348,6 +382,7 @@ void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double
     // the copy stream starts after the work already queued on the plan stream
     KB_CUDA(cudaEventRecord(p->ev_out[kMaxChunks - 1], p->stream));
     KB_CUDA(cudaStreamWaitEvent(p->cstream, p->ev_out[kMaxChunks - 1], 0));
+    tr.mark("start (copy stream)", p->cstream);
     for (int c = 0; c < C; ++c) {
         const int64_t off = c * step, nc = std::min(step, n - off);
         KB_CUDA(cudaMemcpyAsync(p->xyz_d + 3 * off, xyz + 3 * off, sizeof(double) * 3 * nc,
@@ -355,6 +390,7 @@ void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double
         KB_CUDA(cudaMemcpyAsync(p->q_d + off, q + off, sizeof(double) * nc,
                                 cudaMemcpyHostToDevice, p->cstream));
         KB_CUDA(cudaEventRecord(p->ev_in[c], p->cstream));
+        tr.mark("h2d chunk " + std::to_string(c), p->cstream);
     }
     KB_CUDA(cudaMemcpyAsync(p->cbad, p->cflags_h + 2 * kMaxChunks,
                             2 * C * sizeof(unsigned long long), cudaMemcpyHostToDevice, p->stream));
@@ -386,11 +422,14 @@ void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double
                             p->sp + off);
         a.Fpart = p->cFpart + (size_t)c * nb;
         a.fstride = C * nb;
+        tr.mark("sort chunk " + std::to_string(c), p->stream);
         kb::launch_spread_fwd(a, kb::SPREAD_PARTICLES, true, p->stream);
         ++p->launches;
+        tr.mark("spread chunk " + std::to_string(c), p->stream);
     }
     kb::launch_core_sum(g, C * nb, p->cFpart, p->F, p->stream);
     ++p->launches;
+    tr.mark("core sum", p->stream);
     // backward + gather per chunk; its potentials leave while the next runs
     for (int c = 0; c < C; ++c) {
         const int64_t off = c * step, nc = std::min(step, n - off);
@@ -403,9 +442,11 @@ void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double
         kb::launch_bwd_gather(a, kb::GATHER_FROM_B2, p->stream);
         ++p->launches;
         KB_CUDA(cudaEventRecord(p->ev_out[c], p->stream));
+        tr.mark("gather chunk " + std::to_string(c), p->stream);
         KB_CUDA(cudaStreamWaitEvent(p->cstream, p->ev_out[c], 0));
         KB_CUDA(cudaMemcpyAsync(out + off, p->out_d + off, sizeof(double) * nc,
                                 cudaMemcpyDeviceToHost, p->cstream));
+        tr.mark("d2h chunk " + std::to_string(c), p->cstream);
     }
     KB_CUDA(cudaMemcpyAsync(p->cflags_h, p->cbad, 2 * C * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, p->cstream));

@@ -1125,7 +1125,11 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
         __syncthreads();
         if (MONO && MODE != PSI_ONLY && !(GATHER_SKIP & 1) && cb1 - cb0 <= kGatherTab) {
             // cell starts and z axes of the batch in shared memory; each thread
-            // walks its particles in increasing order, so its cell only advances
+            // walks its particles in increasing order, so its cell only advances.
+            // A thread takes two adjacent particles (s, s + 1): in the same cell
+            // for the whole warp (the common case, warp vote) every coefficient
+            // read from shared memory feeds both Horner chains, which halves the
+            // shared-memory wavefronts that bound this loop.
             const int nb = cb1 - cb0;
             for (int e = tid; e <= nb; e += GT) gcst[e] = a.start[cell0 + e];
             for (int e = tid; e < nb; e += GT) gax[e] = a.cellax[2][cb0 + e];
@@ -1133,44 +1137,89 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
             const int s0 = gcst[0], s1 = gcst[nb];
             int cc = 0;
             double tmax = 0.0;
-            double4 pn = s0 + tid < s1 ? ld_rec(a.sp + s0 + tid) : make_double4(0.0, 0.0, 0.0, 0.0);
-            int dn = s0 + tid < s1 ? a.perm[s0 + tid] : 0;
-            for (int s = s0 + tid; s < s1; s += GT) {
-                const double4 p = pn;  // software prefetch of the next particle
-                const int dst = dn;
-                if (s + GT < s1) {
-                    pn = ld_rec(a.sp + s + GT);
-                    dn = a.perm[s + GT];
-                }
-                while (gcst[cc + 1] <= s) ++cc;
-                const double* ps = psi + cc * L3;
-                const double4 x2 = gax[cc];  // (lo, hi, mid, inv)
-                double t[3];
-                t[0] = (p.x - ax0.mid) * ax0.inv;
-                t[1] = (p.y - ax1.mid) * ax1.inv;
-                t[2] = (p.z - x2.z) * x2.w;
-                tmax = fmax(tmax, fmax(fabs(t[0]), fmax(fabs(t[1]), fabs(t[2]))));
+            auto rec = [&](int s) {
+                return s < s1 ? ld_rec(a.sp + s) : make_double4(0.0, 0.0, 0.0, 0.0);
+            };
+            auto idx = [&](int s) { return s < s1 ? a.perm[s] : 0; };
+            int sb = s0 + 2 * tid;
+            double4 pa = rec(sb), pb = rec(sb + 1);
+            int da = idx(sb), db = idx(sb + 1);
+            // nested Horner over the monomial coefficients C[a][b][c] of a cell:
+            // z = sum_a t0^a sum_b t1^b sum_c t2^c C[a][b][c]
+            auto horner1 = [&](const double* ps, const double (&t)[3]) {
                 double z = 0.0;
+#pragma unroll
+                for (int i = L - 1; i >= 0; --i) {
+                    double zb = 0.0;
+#pragma unroll
+                    for (int j = L - 1; j >= 0; --j) {
+                        const double* row = ps + (i * L + j) * L;
+                        double zc = row[L - 1];
+#pragma unroll
+                        for (int k = L - 2; k >= 0; --k) zc = fma(zc, t[2], row[k]);
+                        zb = fma(zb, t[1], zc);
+                    }
+                    z = fma(z, t[0], zb);
+                }
+                return z;
+            };
+            // warp-uniform trip count (lane 0 holds the warp's lowest pair)
+            for (int wb = s0 + 64 * (tid >> 5); wb < s1; wb += 2 * GT, sb += 2 * GT) {
+                const double4 p0 = pa, p1 = pb;  // software prefetch of the next pair
+                const int d0 = da, d1 = db;
+                if (sb + 2 * GT < s1) {
+                    pa = rec(sb + 2 * GT);
+                    pb = rec(sb + 2 * GT + 1);
+                    da = idx(sb + 2 * GT);
+                    db = idx(sb + 2 * GT + 1);
+                }
+                const bool has0 = sb < s1, has1 = sb + 1 < s1;
+                while (gcst[cc + 1] <= min(sb, s1 - 1)) ++cc;
+                int cc1 = cc;
+                while (gcst[cc1 + 1] <= min(sb + 1, s1 - 1)) ++cc1;
+                const double4 xa = gax[cc], xb = gax[cc1];  // (lo, hi, mid, inv)
+                double ta[3], tb[3];
+                ta[0] = (p0.x - ax0.mid) * ax0.inv;
+                ta[1] = (p0.y - ax1.mid) * ax1.inv;
+                ta[2] = (p0.z - xa.z) * xa.w;
+                tb[0] = (p1.x - ax0.mid) * ax0.inv;
+                tb[1] = (p1.y - ax1.mid) * ax1.inv;
+                tb[2] = (p1.z - xb.z) * xb.w;
+                if (has0) tmax = fmax(tmax, fmax(fabs(ta[0]), fmax(fabs(ta[1]), fabs(ta[2]))));
+                if (has1) tmax = fmax(tmax, fmax(fabs(tb[0]), fmax(fabs(tb[1]), fabs(tb[2]))));
+                double za, zb2;
                 if (GATHER_SKIP & 2) {
-                    z = t[0] + t[1] + t[2] + ps[0];
-                } else {
-                    // ps = monomial coefficients C[a][b][c] of this cell's potential:
-                    // z = sum_a t0^a sum_b t1^b sum_c t2^c C[a][b][c] (nested Horner)
+                    za = ta[0] + ta[1] + ta[2] + psi[cc * L3];
+                    zb2 = tb[0] + tb[1] + tb[2] + psi[cc1 * L3];
+                } else if (__all_sync(0xffffffffu, cc1 == cc)) {
+                    const double* ps = psi + cc * L3;
+                    za = 0.0;
+                    zb2 = 0.0;
 #pragma unroll
                     for (int i = L - 1; i >= 0; --i) {
-                        double zb = 0.0;
+                        double ya = 0.0, yb = 0.0;
 #pragma unroll
                         for (int j = L - 1; j >= 0; --j) {
                             const double* row = ps + (i * L + j) * L;
-                            double zc = row[L - 1];
+                            double xa_ = row[L - 1], xb_ = xa_;
 #pragma unroll
-                            for (int k = L - 2; k >= 0; --k) zc = fma(zc, t[2], row[k]);
-                            zb = fma(zb, t[1], zc);
+                            for (int k = L - 2; k >= 0; --k) {
+                                const double ck = row[k];
+                                xa_ = fma(xa_, ta[2], ck);
+                                xb_ = fma(xb_, tb[2], ck);
+                            }
+                            ya = fma(ya, ta[1], xa_);
+                            yb = fma(yb, tb[1], xb_);
                         }
-                        z = fma(z, t[0], zb);
+                        za = fma(za, ta[0], ya);
+                        zb2 = fma(zb2, tb[0], yb);
                     }
+                } else {
+                    za = horner1(psi + cc * L3, ta);
+                    zb2 = horner1(psi + cc1 * L3, tb);
                 }
-                a.out[dst] = z - corr;
+                if (has0) a.out[d0] = za - corr;
+                if (has1) a.out[d1] = zb2 - corr;
             }
             // tensor_weights' out-of-cell check, |t| <= 1 + 2e-12 (slack 1e-12 of the width)
             if (__ballot_sync(0xffffffffu, !(tmax <= 1.0 + 2e-12)) && (tid & 31) == 0)

@@ -43,6 +43,8 @@ def args_():
     p.add_argument("--no-extras", action="store_true")
     p.add_argument("--slab", action="store_true",
                    help="use the z-slab path (SlabPlan + NCCL core all-reduce) even on 1 GPU")
+    p.add_argument("--rank-grid", default=None,
+                   help="P0xP1xP2 device grid of cell blocks for N > 1 (default 1x1xN: z-slabs)")
     return p.parse_args()
 
 
@@ -277,7 +279,8 @@ def run_ours(a):
     if slab:
         from paper_2601_18838_b200.dist import SlabPlan
 
-        plan = SlabPlan(w, rank, world, device=local)
+        dims = tuple(int(v) for v in a.rank_grid.split("x")) if a.rank_grid else None
+        plan = SlabPlan(w, rank, world, device=local, dims=dims)
         step, e2e_step, launches, meta = plan.bench_callables()
     else:
         plan = KpmePlan(w.cfg, w.grid, w.order, w.dec, w.n, device=local)
@@ -385,7 +388,8 @@ def run_ours(a):
         "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded splitmix64 sample_cloud, BASELINE.json config shapes)",
         "config": {**w.describe(), "formulation": "collapsed (term-collapsed SKP core, "
-                   "per-shape chooser)", "parallelism": f"z-slab x{world} (NCCL core all-reduce)" if slab else "1 GPU",
+                   "per-shape chooser)", "parallelism": (f"rank grid {'x'.join(map(str, plan.dims))} of cell blocks "
+                                   f"(NCCL core all-reduce)") if slab else "1 GPU",
                    "l2": "flushed (256 MiB write) before every timed step"},
         "e2e": {"value": w.n / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": 32 * w.n, "d2h_bytes_per_step": 8 * w.n,

@@ -166,6 +166,13 @@ int kpme_gpu_plan_stage_times(kpme_gpu_plan plan, double* ms, int cap,
  * (parallel.hpp:169-176) and allreduce_scalar (parallel.hpp:254-257). */
 int kpme_gpu_plan_create_slab(const kpme_gpu_config* cfg, int64_t max_particles,
                               int z_lo, int z_hi, kpme_gpu_plan* out);
+/* General P0 x P1 x P2 device grids: a plan owning the cell block
+ * [lo[a], hi[a]) on every axis -- one rank of a rank grid that flattens like
+ * cells (RankGrid, parallel.hpp:46-82). The same forward / core all-reduce /
+ * backward halves as slabs; particles outside the block are
+ * KPME_GPU_INVALID_ARGUMENT at the next status check. */
+int kpme_gpu_plan_create_block(const kpme_gpu_config* cfg, int64_t max_particles,
+                               const int lo[3], const int hi[3], kpme_gpu_plan* out);
 int kpme_gpu_plan_core_size(kpme_gpu_plan plan);
 /* sort .. forward contractions: d_core[R^3 + 1] = this slab's partial core */
 int kpme_gpu_plan_forward(kpme_gpu_plan plan, int64_t n, const double* d_xyz,

@@ -94,6 +94,8 @@ def _load():
         "kpme_gpu_dgemm_tn": (C.c_int, [P, C.c_int64, C.c_int64, C.c_int64, P, P, P, C.c_int]),
         "kpme_gpu_plan_create_slab": (C.c_int, [C.POINTER(Config), C.c_int64, C.c_int, C.c_int,
                                                 C.POINTER(P)]),
+        "kpme_gpu_plan_create_block": (C.c_int, [C.POINTER(Config), C.c_int64, C.POINTER(C.c_int),
+                                                 C.POINTER(C.c_int), C.POINTER(P)]),
         "kpme_gpu_plan_core_size": (C.c_int, [P]),
         "kpme_gpu_plan_forward": (C.c_int, [P, C.c_int64, P, P, P]),
         "kpme_gpu_plan_backward": (C.c_int, [P, P, P]),
@@ -120,7 +122,7 @@ EXPORTS = sorted(
         "kpme_gpu_dense_workspace_bytes", "kpme_gpu_kron_matvec_dense",
         "kpme_gpu_plan_axis_operands", "kpme_gpu_dgemm_tn", "kpme_gpu_plan_create_slab",
         "kpme_gpu_plan_core_size", "kpme_gpu_plan_forward", "kpme_gpu_plan_backward",
-        "kpme_gpu_plan_set_host_chunks",
+        "kpme_gpu_plan_set_host_chunks", "kpme_gpu_plan_create_block",
     ]
 )
 

@@ -59,8 +59,13 @@ struct Geometry {
     int R;         // compacted Fourier rows per axis, 2M+1 (the m=0 sine row is 0)
     int ncell;     // K0*K1*K2
     int z_lo, z_hi;  // cell planes along axis 2 owned by this plan (slab)
+    int x_lo, x_hi, y_lo, y_hi;  // cell ranges along axes 0, 1 (a block of a rank grid)
     double inv_diam; // RN(1 / (2 radius)), for the correctly rounded key division
 };
+
+// Columns (c0, c1) of the plan's cell block; column kernels launch
+// block_columns * S CTAs.
+inline int block_columns(const Geometry& g) { return (g.x_hi - g.x_lo) * (g.y_hi - g.y_lo); }
 
 // ---- sort.cu ----------------------------------------------------------------
 struct SortBuffers {

@@ -68,10 +68,11 @@ struct ColumnRange {
 };
 __device__ __forceinline__ ColumnRange column_range(const Geometry& g, int S) {
     ColumnRange r;
-    r.col = blockIdx.x / S;
+    const int lc = blockIdx.x / S, ny = g.y_hi - g.y_lo;  // column of the plan's cell block
     r.seg = blockIdx.x % S;
-    r.c0 = r.col / g.K[1];
-    r.c1 = r.col % g.K[1];
+    r.c0 = g.x_lo + lc / ny;
+    r.c1 = g.y_lo + lc % ny;
+    r.col = r.c0 * g.K[1] + r.c1;
     const int span = g.z_hi - g.z_lo;
     r.zb = g.z_lo + (int)((long long)r.seg * span / S);
     r.ze = g.z_lo + (int)((long long)(r.seg + 1) * span / S);
@@ -1321,7 +1322,7 @@ void launch_spread_mma_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
         attr_done = 1;
     }
     if (smem > 200 * 1024) throw Error(KPME_GPU_INVALID_ARGUMENT, "spread: tile too large");
-    const int grid = a.g.K[0] * a.g.K[1] * a.S;
+    const int grid = block_columns(a.g) * a.S;
     k_spread_mma<L, MONO><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
     KB_CHECK_LAUNCH();
 }
@@ -1342,7 +1343,7 @@ void launch_spread_uv_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
         launch_spread_mma_t<L, true>(a, want_fwd, s);
         return;
     }
-    const int grid = a.g.K[0] * a.g.K[1] * a.S;
+    const int grid = block_columns(a.g) * a.S;
     if (UV_SKIP & 8) {
         static double* scratch = nullptr;
         if (!scratch) {
@@ -1381,7 +1382,7 @@ void launch_gather_t(const ColumnArgs& a0, int mode, cudaStream_t s) {
 #ifdef GATHER_S
     if (mode == GATHER_FROM_B2 && a.B2 == nullptr) a.S = std::max(1, std::min(GATHER_S, a.g.z_hi - a.g.z_lo));
 #endif
-    const int grid = a.g.K[0] * a.g.K[1] * a.S;
+    const int grid = block_columns(a.g) * a.S;
 #ifdef GATHER_CB
     const int cb = std::min(gather_batch(a.g), GATHER_CB);
 #else
@@ -1429,7 +1430,7 @@ void launch_spread_fwd(const ColumnArgs& a, int mode, bool want_fwd, cudaStream_
             default: return launch_spread_mma<8>(a, want_fwd, s);
         }
     }
-    const int grid = a.g.K[0] * a.g.K[1] * a.S;
+    const int grid = block_columns(a.g) * a.S;
     const size_t smem = spread_smem(a.g);
     if (mode == SPREAD_PARTICLES)
         k_spread_fwd<SPREAD_PARTICLES><<<grid, kThreads, smem, s>>>(a, want_fwd ? 1 : 0);
@@ -1461,7 +1462,7 @@ void launch_bwd_gather(const ColumnArgs& a, int mode, cudaStream_t s) {
         case 12: return launch_gather_t<12>(a, mode, s);
         default: break;
     }
-    const int grid = a.g.K[0] * a.g.K[1] * a.S;
+    const int grid = block_columns(a.g) * a.S;
     const int cb = gather_batch(a.g);
     const size_t smem =
         sizeof(double) * ((size_t)a.g.L * a.g.L * a.g.R + (size_t)cb * a.g.L * a.g.L * a.g.L);

@@ -164,7 +164,7 @@ void check_flags(const unsigned long long* f) {
         throw Error(KPME_GPU_INVALID_ARGUMENT,
                     "assign_particles: particle " + std::to_string(f[0]) + " outside the box");
     if (f[1] & 2ull)
-        throw Error(KPME_GPU_INVALID_ARGUMENT, "kpme_gpu: particle outside this plan's slab");
+        throw Error(KPME_GPU_INVALID_ARGUMENT, "kpme_gpu: particle outside this plan's cell block");
     if (f[1] & 1ull) throw Error(KPME_GPU_INVALID_ARGUMENT, "tensor_weights: point outside cell");
 }
 
@@ -329,6 +329,8 @@ void ensure_host_buffers(kpme_gpu_plan p, bool chunked) {
     p->cstart = p->alloc<int32_t>((size_t)kMaxChunks * (g.ncell + 1));
     p->cbad = p->alloc<unsigned long long>(2 * kMaxChunks);
     p->cFpart = p->alloc<double>((size_t)kMaxChunks * nb * ((size_t)g.R * g.R * g.R + 1));
+    KB_CUDA(cudaMemsetAsync(p->cFpart, 0,
+                            sizeof(double) * kMaxChunks * nb * ((size_t)g.R * g.R * g.R + 1), p->stream));
     // [0, 2C): flags read back; [2C, 4C): the reset pattern (ULLONG_MAX, 0)
     KB_CUDA(cudaMallocHost(&p->cflags_h, 4 * kMaxChunks * sizeof(unsigned long long)));
     for (int c = 0; c < kMaxChunks; ++c) {
@@ -479,15 +481,16 @@ void collect_times(kpme_gpu_plan p) {
 }  // namespace
 
 namespace {
-void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, int z_hi,
-                 kpme_gpu_plan* out);
+void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, const int lo[3],
+                 const int hi[3], kpme_gpu_plan* out);
 }
 
 extern "C" int kpme_gpu_plan_create(const kpme_gpu_config* cfg, int64_t max_particles,
                                     kpme_gpu_plan* out) {
     return guarded([&] {
         validate(cfg);
-        create_plan(cfg, max_particles, 0, cfg->counts[2], out);
+        const int lo[3] = {0, 0, 0}, hi[3] = {cfg->counts[0], cfg->counts[1], cfg->counts[2]};
+        create_plan(cfg, max_particles, lo, hi, out);
     });
 }
 
@@ -497,7 +500,20 @@ extern "C" int kpme_gpu_plan_create_slab(const kpme_gpu_config* cfg, int64_t max
         validate(cfg);
         if (z_lo < 0 || z_hi < z_lo || z_hi > cfg->counts[2])
             invalid("kpme_gpu_plan_create_slab: slab outside the cell grid");
-        create_plan(cfg, max_particles, z_lo, z_hi, out);
+        const int lo[3] = {0, 0, z_lo}, hi[3] = {cfg->counts[0], cfg->counts[1], z_hi};
+        create_plan(cfg, max_particles, lo, hi, out);
+    });
+}
+
+extern "C" int kpme_gpu_plan_create_block(const kpme_gpu_config* cfg, int64_t max_particles,
+                                          const int lo[3], const int hi[3], kpme_gpu_plan* out) {
+    return guarded([&] {
+        validate(cfg);
+        if (!lo || !hi) invalid("kpme_gpu_plan_create_block: null bounds");
+        for (int a = 0; a < 3; ++a)
+            if (lo[a] < 0 || hi[a] < lo[a] || hi[a] > cfg->counts[a])
+                invalid("kpme_gpu_plan_create_block: block outside the cell grid");
+        create_plan(cfg, max_particles, lo, hi, out);
     });
 }
 
@@ -523,8 +539,8 @@ extern "C" int kpme_gpu_plan_backward(kpme_gpu_plan p, const double* core, doubl
 }
 
 namespace {
-void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, int z_hi,
-                 kpme_gpu_plan* out) {
+void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, const int lo[3],
+                 const int hi[3], kpme_gpu_plan* out) {
     {
         validate(cfg);
         if (!out) invalid("kpme_gpu_plan_create: null output");
@@ -548,8 +564,12 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, in
             g.M = cfg->modes;
             g.R = 2 * cfg->modes + 1;
             g.ncell = cfg->counts[0] * cfg->counts[1] * cfg->counts[2];
-            g.z_lo = z_lo;
-            g.z_hi = z_hi;
+            g.x_lo = lo[0];
+            g.x_hi = hi[0];
+            g.y_lo = lo[1];
+            g.y_hi = hi[1];
+            g.z_lo = lo[2];
+            g.z_hi = hi[2];
             const int L = g.L, R = g.R;
             const size_t smem_spread =
                 sizeof(double) * ((size_t)L * L * L + (size_t)L * L * R + (size_t)R * L + 64 * 3 * L);
@@ -566,7 +586,8 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, in
 #else
             // z segments per column: enough CTAs for one resident wave (3 per SM
             // for the column kernels), never more than one wave
-            p->S = std::max(1, std::min(std::max(1, g.z_hi - g.z_lo), (3 * 148) / ncol));
+            p->S = std::max(1, std::min(std::max(1, g.z_hi - g.z_lo),
+                                        (3 * 148) / std::max(1, kb::block_columns(g))));
 #endif
 
             const int P = 2 * g.M + 1;
@@ -588,6 +609,11 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, int z_lo, in
             p->colq = p->alloc<double>((size_t)p->S * ncol);
             p->Fpart = p->alloc<double>((size_t)p->S * ncol * ((size_t)R * R * R + 1));
             p->corr = p->alloc<double>(1);
+            // columns outside a block plan's cell block never write their
+            // partials: they stay zero in the fixed-order sums
+            KB_CUDA(cudaMemsetAsync(p->T1, 0, sizeof(double) * p->S * g.n[0] * g.n[1] * R, p->stream));
+            KB_CUDA(cudaMemsetAsync(p->Fpart, 0,
+                                    sizeof(double) * p->S * ncol * ((size_t)R * R * R + 1), p->stream));
             p->sb.cnt = p->alloc<int32_t>(g.ncell);
             p->sb.start = p->alloc<int32_t>(g.ncell + 1);
             p->sb.key = p->alloc<int32_t>(p->cap);

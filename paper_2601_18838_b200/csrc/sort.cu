@@ -54,7 +54,8 @@ __global__ void __launch_bounds__(256) k_keys(Geometry g, int64_t n, const doubl
     const int c0 = axis_cell(p0, g.center[0], g.radius, g.K[0], b, y);
     const int c1 = axis_cell(p1, g.center[1], g.radius, g.K[1], b, y);
     const int c2 = axis_cell(p2, g.center[2], g.radius, g.K[2], b, y);
-    if (c2 < g.z_lo || c2 >= g.z_hi) atomicOr(&bad[1], 2ull);  // not in this slab
+    if (c0 < g.x_lo || c0 >= g.x_hi || c1 < g.y_lo || c1 >= g.y_hi || c2 < g.z_lo || c2 >= g.z_hi)
+        atomicOr(&bad[1], 2ull);  // not in this plan's cell block
     const int k = (c0 * g.K[1] + c1) * g.K[2] + c2;             // CellGrid::flatten
     key[i] = k;
     rank[i] = atomicAdd(&cnt[k], 1);  // provisional slot, fixed up by k_segsort

@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(kHistThreads) k_tile_hist(Geometry g, int64_t 
         const int c0 = axis_cell2(p0, g.center[0], g.radius, g.K[0], b, y);
         const int c1 = axis_cell2(p1, g.center[1], g.radius, g.K[1], b, y);
         const int c2 = axis_cell2(p2, g.center[2], g.radius, g.K[2], b, y);
-        if (c2 < g.z_lo || c2 >= g.z_hi) atomicOr(&bad[1], 2ull);
+        if (c0 < g.x_lo || c0 >= g.x_hi || c1 < g.y_lo || c1 >= g.y_hi || c2 < g.z_lo || c2 >= g.z_hi)
+            atomicOr(&bad[1], 2ull);  // not in this plan's cell block
         key[i] = ((c0 * g.K[1] + c1) << 16) | c2;  // (column, c2) packed
         atomicAdd(&h[c0 * g.K[1] + c1], 1);  // shared-memory counter, order irrelevant
     }

@@ -50,6 +50,47 @@ def axis_cells(x: np.ndarray, center: float, radius: float, k: int) -> np.ndarra
     return np.clip(idx, 0, k - 1)
 
 
+def rank_grid_coords(rank: int, dims) -> tuple[int, int, int]:
+    """RankGrid::unflatten (parallel.hpp:63-70): ranks flatten like cells."""
+    r2 = rank % dims[2]
+    r = rank // dims[2]
+    return r // dims[1], r % dims[1], r2
+
+
+def rank_grid_block(counts, dims, rank: int) -> tuple:
+    """Cell block ((lo0, hi0), (lo1, hi1), (lo2, hi2)) of ``rank`` in a
+    P0 x P1 x P2 device grid: a balanced contiguous split per axis."""
+    c = rank_grid_coords(rank, dims)
+    return tuple(slab_bounds(counts[a], c[a], dims[a]) for a in range(3))
+
+
+def axis_group(rank: int, dims, axis: int) -> list[int]:
+    """RankGrid::axis_group (parallel.hpp:72-81): the ranks agreeing with
+    ``rank`` on every axis but ``axis``, ascending."""
+    c = list(rank_grid_coords(rank, dims))
+    out = []
+    for i in range(dims[axis]):
+        c[axis] = i
+        out.append((c[0] * dims[1] + c[1]) * dims[2] + c[2])
+    return out
+
+
+def route_particles_grid(pos: np.ndarray, grid, dims) -> list[np.ndarray]:
+    """Global indices (ascending) of the particles each rank's cell block
+    owns, for a P0 x P1 x P2 device grid (the exact key arithmetic on every
+    axis)."""
+    pos = np.asarray(pos)
+    cells = [axis_cells(pos[:, a], grid.box.center[a], grid.box.radius, grid.counts[a])
+             for a in range(3)]
+    owner = np.zeros(len(pos), dtype=np.int64)
+    for a in range(3):
+        bounds = np.array([slab_bounds(grid.counts[a], i, dims[a])[1] for i in range(dims[a])])
+        coord = np.searchsorted(bounds, cells[a], side="right")
+        owner = owner * dims[a] + coord
+    world = int(np.prod(dims))
+    return [np.nonzero(owner == r)[0] for r in range(world)]
+
+
 def route_particles(pos: np.ndarray, grid, world: int) -> list[np.ndarray]:
     """Global indices (ascending) of the particles each z-slab owns -- the
     one-off particle distribution step (the paper's all2allv),
@@ -86,18 +127,28 @@ class SlabDriver:
 
 class SlabPlan:
     """Bench-facing wrapper: routes the workload's particles to this rank's
-    slab, builds the slab plan and exposes the timed callables."""
+    slab (or, with ``dims = (P0, P1, P2)``, to its cell block of a general
+    device grid, ranks flattened like RankGrid, parallel.hpp:46-82), builds
+    the plan and exposes the timed callables. The exchange is the same single
+    core all-reduce for every grid shape."""
 
-    def __init__(self, w, rank: int, world: int, device: int = 0, group=None):
+    def __init__(self, w, rank: int, world: int, device: int = 0, group=None, dims=None):
         from .plan import KpmePlan
 
         self.w, self.rank, self.world = w, rank, world
-        self.routes = route_particles(w.data.cloud.positions, w.grid, world)
+        self.dims = tuple(dims) if dims is not None else (1, 1, world)
+        if int(np.prod(self.dims)) != world:
+            raise ValueError(f"rank grid {self.dims} does not have {world} ranks")
+        if self.dims == (1, 1, world):
+            self.routes = route_particles(w.data.cloud.positions, w.grid, world)
+        else:
+            self.routes = route_particles_grid(w.data.cloud.positions, w.grid, self.dims)
         self.idx = self.routes[rank]
-        self.z = slab_bounds(w.grid.counts[2], rank, world)
+        self.block = rank_grid_block(w.grid.counts, self.dims, rank)
+        self.z = self.block[2]
         dev = torch.device("cuda", device)
         self.plan = KpmePlan(w.cfg, w.grid, w.order, w.dec, max(1, len(self.idx)), device=device,
-                             slab=self.z)
+                             block=self.block)
         self.driver = SlabDriver(self.plan, group, dev)
         pos = w.data.cloud.positions[self.idx]
         q = w.data.charges.values[self.idx]
@@ -151,7 +202,8 @@ class SlabPlan:
     def bench_callables(self):
         launches = self.plan.launches()
         self.capture()
-        meta = {"slab_z": list(self.z), "local_particles": int(len(self.idx)),
+        meta = {"rank_grid": list(self.dims), "cell_block": [list(b) for b in self.block],
+                "local_particles": int(len(self.idx)),
                 "exchange": f"all_reduce of {self.plan.core_size()} doubles per step",
                 "cuda_graph": self.graph is not None}
         if self.graph_error:

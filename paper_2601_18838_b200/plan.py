@@ -36,7 +36,8 @@ class KpmePlan:
 
     def __init__(self, cfg: EwaldConfig, grid: CellGrid, order: int, dec: SkpDecomposition,
                  max_particles: int, opt: KpmeOptions | None = None, device: int = 0,
-                 formulation: str = "auto", slab: tuple | None = None):
+                 formulation: str = "auto", slab: tuple | None = None,
+                 block: tuple | None = None):
         if dec.modes != cfg.modes:
             raise ValueError("kpme_apply: decomposition mode bound mismatch")
         self.cfg, self.grid, self.order, self.dec = cfg, grid, order, dec
@@ -44,9 +45,15 @@ class KpmePlan:
         self.max_particles = int(max_particles)
         self._c, self._keep = make_config(cfg, grid, order, dec, opt, device, formulation)
         self._h = C.c_void_p()
-        self.slab = slab
+        self.slab, self.block = slab, block
         with torch.cuda.device(device):
-            if slab is None:
+            if block is not None:
+                # cell block ((lo0, hi0), (lo1, hi1), (lo2, hi2)) of a rank grid
+                lo = (C.c_int * 3)(*[int(b[0]) for b in block])
+                hi = (C.c_int * 3)(*[int(b[1]) for b in block])
+                check(lib.kpme_gpu_plan_create_block(C.byref(self._c), self.max_particles, lo, hi,
+                                                     C.byref(self._h)))
+            elif slab is None:
                 check(lib.kpme_gpu_plan_create(C.byref(self._c), self.max_particles,
                                                C.byref(self._h)))
             else:

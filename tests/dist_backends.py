@@ -28,8 +28,14 @@ def lagrange_rows(order, lo, hi, y):
 
 
 class CpuCollapsedSlab:
-    def __init__(self, pb, z_lo, z_hi):
+    """z_lo, z_hi: the slab; block (optional): the rank's cell block
+    ((lo0, hi0), (lo1, hi1), (lo2, hi2)) of a general device grid, checked
+    like the GPU plan checks it (the mesh keeps full x / y extent: cells
+    outside the block simply stay empty)."""
+
+    def __init__(self, pb, z_lo, z_hi, block=None):
         self.pb, self.z_lo, self.z_hi = pb, z_lo, z_hi
+        self.block = block
         M, L = pb.modes, pb.order
         self.R = 2 * M + 1
         K = pb.counts
@@ -65,6 +71,10 @@ class CpuCollapsedSlab:
         pb, L = self.pb, self.pb.order
         c = [axis_cells(xyz[:, a], pb.center[a], pb.radius, pb.counts[a]) for a in range(3)]
         assert ((c[2] >= self.z_lo) & (c[2] < self.z_hi)).all(), "particle outside the slab"
+        if self.block is not None:
+            for a in range(2):
+                lo, hi = self.block[a]
+                assert ((c[a] >= lo) & (c[a] < hi)).all(), "particle outside the cell block"
         w = []
         for a in range(3):
             lo = pb.center[a] - pb.radius + 2.0 * pb.radius * c[a] / pb.counts[a]

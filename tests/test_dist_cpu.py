@@ -62,6 +62,40 @@ def _collapsed_worker(rank, world, port, res):
     dist.destroy_process_group()
 
 
+def _grid_worker(rank, world, port, res):
+    """Collapsed path on a general device grid: rank grids (2, 1, 1) and
+    (1, 2, 1) -- cell blocks split along x / y, same single core all-reduce."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    _init(rank, world, port)
+    from oracle.binding import CpuKpme, make_problem
+    from paper_2601_18838_b200.api import Box3, build_cell_grid
+    from paper_2601_18838_b200.dist import SlabDriver, rank_grid_block, route_particles_grid
+    from tests.dist_backends import CpuCollapsedSlab
+
+    oracle = CpuKpme("oracle")
+    pb = make_problem(oracle, n=400, counts=(4, 3, 2), order=4, modes=3, eps=1e-9, seed=5,
+                      charges="neutral")
+    grid = build_cell_grid(Box3(pb.center, pb.radius), pb.counts)
+    ref = oracle.kpme_apply(pb) if rank == 0 else None
+    for dims in ((2, 1, 1), (1, 2, 1)):
+        idx = route_particles_grid(pb.pos, grid, dims)[rank]
+        block = rank_grid_block(pb.counts, dims, rank)
+        drv = SlabDriver(CpuCollapsedSlab(pb, block[2][0], block[2][1], block), device="cpu")
+        out = torch.zeros(len(idx), dtype=torch.float64)
+        drv.apply(torch.as_tensor(pb.pos[idx]), torch.as_tensor(pb.q[idx]), out)
+        parts = [None] * world
+        dist.all_gather_object(parts, (idx, out.numpy()))
+        if rank == 0:
+            z = np.zeros(len(pb.q))
+            for i, v in parts:
+                z[i] = v
+            res[str(dims)] = (float(np.linalg.norm(z - ref) / np.linalg.norm(ref)),
+                              int(sum(len(i) for i, _ in parts)))
+    dist.destroy_process_group()
+
+
 def _dense_worker(rank, world, port, res):
     import sys
 
@@ -135,3 +169,42 @@ def test_dense_strategies_gloo_world2():
         for s, e in rank_errs.items():
             assert e <= 1e-12, (s, e)
     assert res["choice"] in ("reduce_scatter", "rank_split", "alltoall")
+
+
+def test_rank_grid_routing_matches_reference_sort(oracle):
+    """General P0 x P1 x P2 device grids: every particle is routed once, to
+    the rank whose cell block holds its cell (bit-exact cell arithmetic);
+    blocks tile the grid and ranks flatten like RankGrid (parallel.hpp:46-82)."""
+    from oracle.binding import make_problem
+    from paper_2601_18838_b200.api import Box3, build_cell_grid
+    from paper_2601_18838_b200.dist import axis_group, rank_grid_block, route_particles_grid
+
+    pb = make_problem(oracle, n=5000, counts=(5, 4, 7), order=4, modes=2, eps=1e-6, seed=6)
+    grid = build_cell_grid(Box3(pb.center, pb.radius), pb.counts)
+    perm, start = oracle.assign_particles(pb.center, pb.radius, pb.counts, pb.pos)
+    cell_of = np.empty(len(perm), np.int64)
+    for c in range(len(start) - 1):
+        cell_of[perm[start[c]:start[c + 1]]] = c
+    K = pb.counts
+    c0, c1, c2 = cell_of // (K[1] * K[2]), (cell_of // K[2]) % K[1], cell_of % K[2]
+    for dims in ((2, 2, 2), (1, 4, 1), (3, 1, 2), (1, 1, 8)):
+        routes = route_particles_grid(pb.pos, grid, dims)
+        assert sum(len(r) for r in routes) == len(perm)
+        cells = 0
+        for r, idx in enumerate(routes):
+            b = rank_grid_block(K, dims, r)
+            cells += np.prod([hi - lo for lo, hi in b])
+            for a, ca in enumerate((c0, c1, c2)):
+                assert ((ca[idx] >= b[a][0]) & (ca[idx] < b[a][1])).all()
+            assert (np.diff(idx) > 0).all()
+        assert cells == K[0] * K[1] * K[2]
+    assert axis_group(5, (2, 2, 2), 1) == [5, 7]
+    assert axis_group(5, (2, 2, 2), 0) == [1, 5]
+
+
+def test_collapsed_rank_grids_gloo_world2():
+    res = _run(_grid_worker)
+    for dims in ("(2, 1, 1)", "(1, 2, 1)"):
+        rel, covered = res[dims]
+        assert covered == 400
+        assert rel <= 1e-10, (dims, rel)

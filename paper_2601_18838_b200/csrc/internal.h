@@ -126,6 +126,9 @@ struct ColumnArgs {
     int mono;
     // per-axis cell tables (axis_lo, axis_hi, midpoint, 1/half-width), K_a each
     const double4* cellax[3];
+    // monomial gather: a thread takes two adjacent particles (pays off when
+    // cells are full enough that a warp's pairs rarely straddle a cell)
+    int gpairs;
 };
 enum SpreadMode { SPREAD_PARTICLES = 0, SPREAD_FROM_CELLS = 1 };
 enum GatherMode { GATHER_FROM_B2 = 0, GATHER_FROM_CELLS = 1, PSI_ONLY = 2 };

@@ -978,6 +978,9 @@ template <int L, int MODE, bool MONO>
 #ifndef GATHER_SKIP
 #define GATHER_SKIP 0  // profiling ablations only: 1 particle loop, 2 Horner
 #endif
+#ifndef GATHER_PAIRS
+#define GATHER_PAIRS 1  // allow two adjacent particles per thread (ColumnArgs::gpairs)
+#endif
 #ifndef GATHER_MINB
 #define GATHER_MINB (512 / GT)
 #endif
@@ -1124,7 +1127,59 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
             }
         }
         __syncthreads();
-        if (MONO && MODE != PSI_ONLY && !(GATHER_SKIP & 1) && cb1 - cb0 <= kGatherTab) {
+        if (MONO && MODE != PSI_ONLY && !(GATHER_SKIP & 1) && cb1 - cb0 <= kGatherTab && !(GATHER_PAIRS && a.gpairs)) {
+            // cell starts and z axes of the batch in shared memory; each thread
+            // walks its particles in increasing order, so its cell only advances
+            const int nb = cb1 - cb0;
+            for (int e = tid; e <= nb; e += GT) gcst[e] = a.start[cell0 + e];
+            for (int e = tid; e < nb; e += GT) gax[e] = a.cellax[2][cb0 + e];
+            __syncthreads();
+            const int s0 = gcst[0], s1 = gcst[nb];
+            int cc = 0;
+            double tmax = 0.0;
+            double4 pn = s0 + tid < s1 ? ld_rec(a.sp + s0 + tid) : make_double4(0.0, 0.0, 0.0, 0.0);
+            int dn = s0 + tid < s1 ? a.perm[s0 + tid] : 0;
+            for (int s = s0 + tid; s < s1; s += GT) {
+                const double4 p = pn;  // software prefetch of the next particle
+                const int dst = dn;
+                if (s + GT < s1) {
+                    pn = ld_rec(a.sp + s + GT);
+                    dn = a.perm[s + GT];
+                }
+                while (gcst[cc + 1] <= s) ++cc;
+                const double* ps = psi + cc * L3;
+                const double4 x2 = gax[cc];  // (lo, hi, mid, inv)
+                double t[3];
+                t[0] = (p.x - ax0.mid) * ax0.inv;
+                t[1] = (p.y - ax1.mid) * ax1.inv;
+                t[2] = (p.z - x2.z) * x2.w;
+                tmax = fmax(tmax, fmax(fabs(t[0]), fmax(fabs(t[1]), fabs(t[2]))));
+                double z = 0.0;
+                if (GATHER_SKIP & 2) {
+                    z = t[0] + t[1] + t[2] + ps[0];
+                } else {
+                    // ps = monomial coefficients C[a][b][c] of this cell's potential:
+                    // z = sum_a t0^a sum_b t1^b sum_c t2^c C[a][b][c] (nested Horner)
+#pragma unroll
+                    for (int i = L - 1; i >= 0; --i) {
+                        double zb = 0.0;
+#pragma unroll
+                        for (int j = L - 1; j >= 0; --j) {
+                            const double* row = ps + (i * L + j) * L;
+                            double zc = row[L - 1];
+#pragma unroll
+                            for (int k = L - 2; k >= 0; --k) zc = fma(zc, t[2], row[k]);
+                            zb = fma(zb, t[1], zc);
+                        }
+                        z = fma(z, t[0], zb);
+                    }
+                }
+                a.out[dst] = z - corr;
+            }
+            // tensor_weights' out-of-cell check, |t| <= 1 + 2e-12 (slack 1e-12 of the width)
+            if (__ballot_sync(0xffffffffu, !(tmax <= 1.0 + 2e-12)) && (tid & 31) == 0)
+                atomicOr(&a.bad[1], 1ull);
+        } else if (MONO && MODE != PSI_ONLY && !(GATHER_SKIP & 1) && cb1 - cb0 <= kGatherTab) {
             // cell starts and z axes of the batch in shared memory; each thread
             // walks its particles in increasing order, so its cell only advances.
             // A thread takes two adjacent particles (s, s + 1): in the same cell

@@ -9,6 +9,10 @@ cat gpurun_out/bench.json
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > /dev/null 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/ncu_launch.log 2>&1
+# the bench's list mixes full-size launches (value) with the e2e path's
+# per-chunk launches; the device path alone, for per-kernel times:
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_step.csv \
+    python scripts/profile_step.py cfg3 3 > gpurun_out/ncu_launch_step.log 2>&1
 python scripts/profile_step.py cfg3 2 > /dev/null 2>&1 || exit 1
 ncu --set full --clock-control none --import-source on \
     -k regex:"k_spread|k_bwd_gather|k_col_scatter|k_z_sort|k_tile_hist|k_col_scan|k_core_sum" -c 7 \

@@ -172,6 +172,27 @@ __global__ void k_concat_terms(int nterms, int n, const double* __restrict__ C,
     }
 }
 
+// Ccat[k][z'][r' n2 + z] = C_{k tps + r'}[z'][z]: the term-concatenated
+// last-pass operand of every split k (tps terms each) in one launch.
+__global__ void k_concat_splits(int nterms, int tps, int n, const double* __restrict__ C,
+                                double* __restrict__ Ccat) {
+    const int64_t total = (int64_t)nterms * n * n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int z = (int)(e % n), zp = (int)((e / n) % n), r = (int)(e / ((int64_t)n * n));
+        const int k = r / tps, rl = r % tps;
+        Ccat[(int64_t)k * tps * n * n + (int64_t)zp * tps * n + (int64_t)rl * n + z] = C[e];
+    }
+}
+
+// Largest divisor of cr not above want: equal term counts per split, so the
+// split GEMMs are one batched launch.
+int even_splits(int want, int cr) {
+    for (int d = std::min(want, cr); d > 1; --d)
+        if (cr % d == 0) return d;
+    return 1;
+}
+
 int chunk_terms(int n0, int n1, int n2, int nterms) {
     // keep the term-stacked intermediates (two per term) within ~16 GB of HBM
     const double mesh = 8.0 * n0 * n1 * n2;
@@ -255,23 +276,20 @@ void kron_matvec_dense(cudaStream_t s, int n0, int n1, int n2, int nterms, const
         dgemm_tn_batched(s, (int64_t)n2 * n0, n1, n1, t1, mesh, B + (int64_t)r0 * n1 * n1,
                          (int64_t)n1 * n1, t2, mesh, cr, false);
         // pass C over (term, z): y[(x',y')][z'] (+)= sum_{r,z} t2[r][z][(x',y')] C_r[z'][z]
-        const int sp = std::min(splits, cr);
+        const int sp = even_splits(splits, cr);
         if (sp <= 1) {
             k_concat_terms<<<148 * 4, 256, 0, s>>>(cr, n2, C + (int64_t)r0 * n2 * n2, ccat);
             KB_CHECK_LAUNCH();
             dgemm_tn(s, (int64_t)n0 * n1, n2, (int64_t)cr * n2, t2, ccat, y, r0 > 0);
         } else {
-            // split-K over terms: split k covers terms [k*cr/sp, (k+1)*cr/sp), with its own
-            // concatenated operand [z'][(tb-ta) n2] at ccat + ta n2^2
-            for (int k = 0; k < sp; ++k) {
-                const int ta = k * cr / sp, tb = (k + 1) * cr / sp;
-                double* ck = ccat + (int64_t)ta * n2 * n2;
-                k_concat_terms<<<148 * 2, 256, 0, s>>>(tb - ta, n2,
-                                                       C + (int64_t)(r0 + ta) * n2 * n2, ck);
-                KB_CHECK_LAUNCH();
-                dgemm_tn(s, (int64_t)n0 * n1, n2, (int64_t)(tb - ta) * n2, t2 + ta * mesh, ck,
-                         part + k * mesh, false);
-            }
+            // split-K over terms, one batched launch: split k covers terms
+            // [k tps, (k+1) tps) with its concatenated operand [z'][tps n2]
+            // at ccat + k tps n2^2; partial sums summed in split order below
+            const int tps = cr / sp;
+            k_concat_splits<<<148 * 4, 256, 0, s>>>(cr, tps, n2, C + (int64_t)r0 * n2 * n2, ccat);
+            KB_CHECK_LAUNCH();
+            dgemm_tn_batched(s, (int64_t)n0 * n1, n2, (int64_t)tps * n2, t2, tps * mesh, ccat,
+                             (int64_t)tps * n2 * n2, part, mesh, sp, false);
             k_sum_splits<<<148 * 8, 256, 0, s>>>(mesh, sp, part, y, r0 > 0 ? 1 : 0);
             KB_CHECK_LAUNCH();
         }

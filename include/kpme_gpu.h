@@ -133,7 +133,7 @@ int kpme_gpu_plan_set_stream(kpme_gpu_plan plan, void* stream);
 int kpme_gpu_plan_execute(kpme_gpu_plan plan, int64_t n, const double* xyz,
                           const double* q, double* potentials);
 /* Chunk count of kpme_gpu_plan_execute: -1 automatic (one chunk per ~1/3 M
- * particles, at most 4), 1 = unpipelined, else 2..8. */
+ * particles, at most 3), 1 = unpipelined, else 2..8. */
 int kpme_gpu_plan_set_host_chunks(kpme_gpu_plan plan, int chunks);
 /* Device buffers, stream-ordered. flags & KPME_GPU_DEFER_CHECKS skips the
  * stream synchronisation that reports invalid particles; call

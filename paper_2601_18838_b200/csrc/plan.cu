@@ -321,9 +321,10 @@ void backward_half(kpme_gpu_plan p, const double* core, double* out) {
 int chunk_count(kpme_gpu_plan p, int64_t n) {
     if (p->form == KPME_GPU_FORM_DENSE || p->g.L > 8) return 1;
     int c = p->host_chunks;
-    // automatic: ~1/3 M particles per chunk, at most 4 (measured on B200 at
-    // configs 3 and 4: more chunks add fixed per-chunk sort/spread cost)
-    if (c < 0) c = (int)std::min<int64_t>(4, std::max<int64_t>(1, (n + 166667) / 333333));
+    // automatic: ~1/3 M particles per chunk, at most 3 (measured on B200 with
+    // the decreasing chunk sizes, configs 3 and 4: more chunks add fixed
+    // per-chunk sort/spread/gather cost)
+    if (c < 0) c = (int)std::min<int64_t>(3, std::max<int64_t>(1, (n + 166667) / 333333));
     return std::max(1, std::min(c, kMaxChunks));
 }
 
@@ -385,10 +386,29 @@ void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double
                      int C) {
     const kb::Geometry& g = p->g;
     ChunkTrace tr;
-    // chunk boundaries on 2048-particle tiles keep every per-chunk slice as
-    // aligned as the buffers' bases
-    const int64_t step = ((n + C - 1) / C + 2047) / 2048 * 2048;
-    C = (int)((n + step - 1) / step);
+    // Chunk sizes decrease linearly (weights C, C-1, ..., 1): the last chunk,
+    // whose sort and spread cannot hide under a copy, is the smallest, and
+    // the gathers run smallest chunk first, so the potentials start leaving
+    // early. Boundaries on 2048-particle tiles keep every slice as aligned as
+    // the buffers' bases. KPME_GPU_EVEN_CHUNKS=1: equal chunks, in order.
+    static const bool even = [] {
+        const char* e = getenv("KPME_GPU_EVEN_CHUNKS");
+        return e && *e == '1';
+    }();
+    int64_t bnd[kMaxChunks + 1];
+    {
+        const int64_t wsum = even ? C : (int64_t)C * (C + 1) / 2;
+        int64_t acc = 0, w = 0;
+        bnd[0] = 0;
+        int k = 0;
+        for (int c = 0; c < C; ++c) {
+            w += even ? 1 : C - c;
+            acc = std::min(n, (n * w / wsum + 2047) / 2048 * 2048);
+            if (acc > bnd[k]) bnd[++k] = acc;
+        }
+        if (bnd[k] < n) bnd[++k] = n;
+        C = k;
+    }
     const int nb = p->S * g.K[0] * g.K[1];
     p->launches = 0;
     // the copy stream starts after the work already queued on the plan stream
@@ -396,7 +416,7 @@ void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double
     KB_CUDA(cudaStreamWaitEvent(p->cstream, p->ev_out[kMaxChunks - 1], 0));
     tr.mark("start (copy stream)", p->cstream);
     for (int c = 0; c < C; ++c) {
-        const int64_t off = c * step, nc = std::min(step, n - off);
+        const int64_t off = bnd[c], nc = bnd[c + 1] - bnd[c];
         KB_CUDA(cudaMemcpyAsync(p->xyz_d + 3 * off, xyz + 3 * off, sizeof(double) * 3 * nc,
                                 cudaMemcpyHostToDevice, p->cstream));
         KB_CUDA(cudaMemcpyAsync(p->q_d + off, q + off, sizeof(double) * nc,
@@ -407,7 +427,7 @@ void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double
     KB_CUDA(cudaMemcpyAsync(p->cbad, p->cflags_h + 2 * kMaxChunks,
                             2 * C * sizeof(unsigned long long), cudaMemcpyHostToDevice, p->stream));
     auto chunk_args = [&](int c, kb::SortBuffers& sb) {
-        const int64_t off = c * step;
+        const int64_t off = bnd[c];
         sb = p->sb;
         sb.start = p->cstart + (size_t)c * (g.ncell + 1);
         sb.perm = p->sb.perm + off;
@@ -422,7 +442,7 @@ void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double
     };
     // forward: per chunk sort + spread into its block of partial cores
     for (int c = 0; c < C; ++c) {
-        const int64_t off = c * step, nc = std::min(step, n - off);
+        const int64_t off = bnd[c], nc = bnd[c + 1] - bnd[c];
         KB_CUDA(cudaStreamWaitEvent(p->stream, p->ev_in[c], 0));
         kb::SortBuffers sb;
         kb::ColumnArgs a = chunk_args(c, sb);
@@ -443,8 +463,9 @@ void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double
     ++p->launches;
     tr.mark("core sum", p->stream);
     // backward + gather per chunk; its potentials leave while the next runs
-    for (int c = 0; c < C; ++c) {
-        const int64_t off = c * step, nc = std::min(step, n - off);
+    for (int i = 0; i < C; ++i) {
+        const int c = even ? i : C - 1 - i;
+        const int64_t off = bnd[c], nc = bnd[c + 1] - bnd[c];
         kb::SortBuffers sb;
         kb::ColumnArgs a = chunk_args(c, sb);
         a.out = p->out_d + off;
@@ -470,7 +491,7 @@ void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double
         if (p->cflags_h[2 * c] != ULLONG_MAX)
             throw Error(KPME_GPU_INVALID_ARGUMENT,
                         "assign_particles: particle " +
-                            std::to_string(c * step + (int64_t)p->cflags_h[2 * c]) +
+                            std::to_string(bnd[c] + (int64_t)p->cflags_h[2 * c]) +
                             " outside the box");
     unsigned long long any = 0;
     for (int c = 0; c < C; ++c) any |= p->cflags_h[2 * c + 1];

@@ -330,6 +330,31 @@ def test_e2e_water_vs_oracle(oracle, molecules, K):
     assert rel(zh, zd) <= 1e-13
 
 
+@pytest.mark.parametrize("n,chunks", [(2049, 8), (4096, 3), (1, 4), (0, 2)])
+def test_host_path_chunk_edges(oracle, n, chunks):
+    """Chunk boundaries at and around the 2048-particle tile: empty chunks are
+    dropped, a chunk of one particle works, n = 0 returns nothing."""
+    from oracle.binding import make_problem
+
+    pb = make_problem(oracle, n=max(n, 1), counts=(3, 4, 5), order=5, modes=3, eps=1e-8, seed=n,
+                      charges="neutral")
+    pos, q = np.array(pb.pos)[:n], np.array(pb.q)[:n]
+    plan = plan_for(pb, n=max(n, 1))
+    plan.set_host_chunks(chunks)
+    zh = plan.execute_host(pos, q)
+    assert zh.shape == (n,)
+    if n == 0:
+        return
+    pb.pos, pb.q = pos, q
+    ref = oracle.kpme_apply(pb)
+    if n > 1:
+        assert rel(zh, ref) <= E2E_TOL
+    else:
+        assert abs(zh[0] - ref[0]) <= 1e-12 * max(1.0, abs(ref[0]))
+    zd = plan.execute(dev(pos), dev(q)).cpu().numpy()
+    assert rel(zh, zd) <= 1e-13
+
+
 def test_e2e_cfg4_properties():
     """Config 4 (3M sites) at full size: size-independent properties --
     symmetry <q1, H q2> = <q2, H q1> of the SPD-like operator S^T H S - c 11^T,

@@ -759,11 +759,12 @@ __host__ __device__ constexpr size_t spread_uv_smem_doubles(int R, int n2) {
 }
 
 #ifndef UV_SKIP
-#define UV_SKIP 0  // profiling ablations only: 1 k-step loop, 2 per-cell contraction, 4 epilogue,
-                   // 8 raw per-cell fragments to a scratch buffer
+#define UV_SKIP 0  // profiling ablations only: 1 k-step loop, 2 per-cell drain + contraction,
+                   // 4 epilogue, 8 raw per-cell fragments to a scratch buffer, 16 contraction only
 #endif
 __device__ double* uv_scratch;
-template <int L>
+// RTM: n-tiles of the W2 contraction held in registers (2: R <= 16, 4: R <= 32).
+template <int L, int RTM>
 __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, int want_fwd) {
     using M = UvMap<L>;
     constexpr int L2 = M::L2, L3 = L2 * L, NT = M::NT, MT2 = M::MT2, KS2 = M::KS2, LDK = M::LDK;
@@ -806,6 +807,13 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, in
     const bool use_t2 = gg < L, multi = M::multi(gg);
     double tmax = 0.0;  // largest |t| seen (out-of-cell check at the end)
     double qsum = 0.0;
+    // the warp's partial of T1 = sum over its cells of ph_c . W2_c, accumulated
+    // by the contraction DMMAs in registers across cells (no per-cell drain)
+    double t1acc[MT2][RTM][2];
+#pragma unroll
+    for (int mt = 0; mt < MT2; ++mt)
+#pragma unroll
+        for (int t = 0; t < RTM; ++t) t1acc[mt][t][0] = t1acc[mt][t][1] = 0.0;
     __syncthreads();
     auto cstart = [&](int c2) { return cst_ok ? cst[c2 - cr.zb] : a.start[col_cell0 + c2]; };
 
@@ -925,7 +933,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, in
         if (a.phi_cells)
             for (int node = lane; node < L3; node += 32)
                 a.phi_cells[(int64_t)(col_cell0 + c2) * L3 + node] = ph[(node / L) * LDK + node % L];
-        if (want_fwd) {
+        if (want_fwd && !(UV_SKIP & 16)) {
             // T1c = ph[(i,j)][k] (MT2*8 x LDK) . W2s[k][r] (LDK x RP)
             double bf[KS2][4];
             const double* w2c = w2s + c2 * L;
@@ -937,27 +945,25 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, in
                     bf[s][t] = (t < RT && k < L && rr < R) ? w2c[rr * n2 + k] : 0.0;
                 }
 #pragma unroll
-            for (int mt = 0; mt < MT2; ++mt) {
-                double c[4][2];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) c[t][0] = c[t][1] = 0.0;
+            for (int mt = 0; mt < MT2; ++mt)
 #pragma unroll
                 for (int s = 0; s < KS2; ++s) {
                     const double af = ph[(mt * 8 + (lane >> 2)) * LDK + s * 4 + (lane & 3)];
 #pragma unroll
-                    for (int t = 0; t < 4; ++t)
-                        if (t < RT) dmma884(c[t], af, bf[s][t]);
+                    for (int t = 0; t < RTM; ++t)
+                        if (t < RT) dmma884(t1acc[mt][t], af, bf[s][t]);
                 }
-#pragma unroll
-                for (int t = 0; t < 4; ++t)
-                    if (t < RT) {
-                        double2* d = reinterpret_cast<double2*>(t1w + (mt * 8 + (lane >> 2)) * RP + t * 8 +
-                                                                2 * (lane & 3));
-                        const double2 o = *d;
-                        *d = make_double2(o.x + c[t][0], o.y + c[t][1]);
-                    }
-            }
         }
+        __syncwarp();
+    }
+    if (want_fwd) {
+#pragma unroll
+        for (int mt = 0; mt < MT2; ++mt)
+#pragma unroll
+            for (int t = 0; t < RTM; ++t)
+                if (t < RT)
+                    *reinterpret_cast<double2*>(t1w + (mt * 8 + (lane >> 2)) * RP + t * 8 + 2 * (lane & 3)) =
+                        make_double2(t1acc[mt][t][0], t1acc[mt][t][1]);
         __syncwarp();
     }
     // tensor_weights' out-of-cell check, |t| <= 1 + 2e-12 (slack 1e-12 of the width)
@@ -1390,7 +1396,9 @@ void launch_spread_uv_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
     const size_t smem = sizeof(double) * spread_uv_smem_doubles<L>(a.g.R, a.g.n[2]);
     static int attr_done = 0;
     if (!attr_done) {
-        KB_CUDA(cudaFuncSetAttribute(k_spread_uv<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        KB_CUDA(cudaFuncSetAttribute(k_spread_uv<L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+        KB_CUDA(cudaFuncSetAttribute(k_spread_uv<L, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      200 * 1024));
         attr_done = 1;
     }
@@ -1406,7 +1414,10 @@ void launch_spread_uv_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
             KB_CUDA(cudaMemcpyToSymbol(uv_scratch, &scratch, sizeof(scratch)));
         }
     }
-    k_spread_uv<L><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+    if (a.g.R <= 16)
+        k_spread_uv<L, 2><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+    else
+        k_spread_uv<L, 4><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
     KB_CHECK_LAUNCH();
 }
 

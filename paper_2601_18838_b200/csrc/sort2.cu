@@ -362,21 +362,15 @@ struct ZWholeLayout {
 };
 constexpr size_t kZWholeMaxSmem = 112 * 1024;  // two CTAs per SM
 
+// Steps 2-5 of the whole-column sort: the column's m records and indices are
+// staged in shared memory in ascending particle order and cnt is zeroed.
 template <int ZB>
-__device__ __forceinline__ void z_sort_whole(const Geometry& g, int col, int cs, int m,
-                                             int64_t n, const int32_t* __restrict__ idx2,
-                                             const double4* __restrict__ rec2,
-                                             int32_t* __restrict__ perm,
-                                             int32_t* __restrict__ start,
-                                             double4* __restrict__ sp, unsigned char* zsm,
-                                             uint64_t* bar, int32_t* wsum) {
+__device__ __forceinline__ void z_whole_body(const Geometry& g, int col, int cs, int m, int64_t n,
+                                             const double4* s_rec, const int32_t* s_idx,
+                                             uint16_t* s_inv, uint8_t* s_z, uint16_t* cnt,
+                                             int32_t* __restrict__ perm, int32_t* __restrict__ start,
+                                             double4* __restrict__ sp, int32_t* wsum) {
     const int K2 = g.K[2], ncol = g.K[0] * g.K[1];
-    const ZWholeLayout L(K2);
-    double4* s_rec = reinterpret_cast<double4*>(zsm + L.rec);
-    int32_t* s_idx = reinterpret_cast<int32_t*>(zsm + L.idx);
-    uint16_t* s_inv = reinterpret_cast<uint16_t*>(zsm + L.inv);
-    uint8_t* s_z = reinterpret_cast<uint8_t*>(zsm + L.z);
-    uint16_t* cnt = reinterpret_cast<uint16_t*>(zsm + L.cnt);  // [K2][kZThreads]
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 #ifdef ZSORT_PROFILE
     long long T[8];
@@ -386,21 +380,6 @@ __device__ __forceinline__ void z_sort_whole(const Geometry& g, int col, int cs,
 #else
 #define ZSTAMP()
 #endif
-    // 1: stage the column with bulk copies (indices from the multiple of 4 at
-    // or below cs, so both ends are 16-byte aligned; idx2 has 4 spare slots)
-    const int cs_al = cs & ~3, m_al = ((cs + m + 3) & ~3) - cs_al;
-    if (tid == 0) {
-        mbar_init(bar, 1);
-        const unsigned brec = 32u * (unsigned)m, bidx = 4u * (unsigned)m_al;
-        mbar_expect_tx(bar, brec + bidx);
-        if (brec) bulk_g2s_pieces(s_rec, rec2 + cs, brec, bar);
-        if (bidx) bulk_g2s_pieces(s_idx, idx2 + cs_al, bidx, bar);
-    }
-    for (int e = tid; e < K2 * kZThreads; e += kZThreads) cnt[e] = 0;
-    __syncthreads();  // barrier initialised before anyone waits on it
-    mbar_wait(bar, 0);
-    ZSTAMP();
-    s_idx += cs - cs_al;
     // 2: per-thread counts over the thread's contiguous slice, kept as 4-bit
     // counters packed in registers (at most 10 particles per thread)
     // four named 64-bit words of 16 counters (c2 < 64); named, not an
@@ -483,6 +462,40 @@ __device__ __forceinline__ void z_sort_whole(const Geometry& g, int col, int cs,
         printf("zsort col %d sm %d m %d: load %lld count %lld scan %lld rank %lld write %lld start %lld\n", col,
                (int)__smid(), m, T[1] - T[0], T[2] - T[1], T[3] - T[2], T[4] - T[3], T[5] - T[4], T[0]);
 #endif
+#undef ZSTAMP
+}
+
+template <int ZB>
+__device__ __forceinline__ void z_sort_whole(const Geometry& g, int col, int cs, int m,
+                                             int64_t n, const int32_t* __restrict__ idx2,
+                                             const double4* __restrict__ rec2,
+                                             int32_t* __restrict__ perm,
+                                             int32_t* __restrict__ start,
+                                             double4* __restrict__ sp, unsigned char* zsm,
+                                             uint64_t* bar, int32_t* wsum) {
+    const int K2 = g.K[2];
+    const ZWholeLayout L(K2);
+    double4* s_rec = reinterpret_cast<double4*>(zsm + L.rec);
+    int32_t* s_idx = reinterpret_cast<int32_t*>(zsm + L.idx);
+    uint16_t* s_inv = reinterpret_cast<uint16_t*>(zsm + L.inv);
+    uint8_t* s_z = reinterpret_cast<uint8_t*>(zsm + L.z);
+    uint16_t* cnt = reinterpret_cast<uint16_t*>(zsm + L.cnt);  // [K2][kZThreads]
+    const int tid = threadIdx.x;
+    // 1: stage the column with bulk copies (indices from the multiple of 4 at
+    // or below cs, so both ends are 16-byte aligned; idx2 has 4 spare slots)
+    const int cs_al = cs & ~3, m_al = ((cs + m + 3) & ~3) - cs_al;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        const unsigned brec = 32u * (unsigned)m, bidx = 4u * (unsigned)m_al;
+        mbar_expect_tx(bar, brec + bidx);
+        if (brec) bulk_g2s_pieces(s_rec, rec2 + cs, brec, bar);
+        if (bidx) bulk_g2s_pieces(s_idx, idx2 + cs_al, bidx, bar);
+    }
+    for (int e = tid; e < K2 * kZThreads; e += kZThreads) cnt[e] = 0;
+    __syncthreads();  // barrier initialised before anyone waits on it
+    mbar_wait(bar, 0);
+    s_idx += cs - cs_al;
+    z_whole_body<ZB>(g, col, cs, m, n, s_rec, s_idx, s_inv, s_z, cnt, perm, start, sp, wsum);
 }
 
 // Chunked fallback for columns above kZCap (or grids whose counters do not
@@ -504,8 +517,14 @@ struct ZLayout {
     }
 };
 
-template <int ZB>
-__device__ __forceinline__ void z_sort_chunked(const Geometry& g, int col, int cs, int m,
+// src(j) is the position in rec2/idx2 of the column's j-th particle in
+// ascending particle order.
+struct ContiguousSrc {
+    int cs;
+    __device__ int64_t operator()(int j) const { return (int64_t)cs + j; }
+};
+template <int ZB, class Src>
+__device__ __forceinline__ void z_sort_chunked(const Geometry& g, int col, int cs, int m, Src src,
                                                int64_t n, const int32_t* __restrict__ idx2,
                                                const double4* __restrict__ rec2,
                                                int32_t* __restrict__ perm,
@@ -523,7 +542,7 @@ __device__ __forceinline__ void z_sort_chunked(const Geometry& g, int col, int c
     for (int e = tid; e < K2; e += kZThreads) zrun[e] = 0;
     __syncthreads();
     // column histogram over c2 (order-free)
-    for (int j = tid; j < m; j += kZThreads) atomicAdd(&zrun[rec_c2(g, ld_rec(rec2 + cs + j))], 1);
+    for (int j = tid; j < m; j += kZThreads) atomicAdd(&zrun[rec_c2(g, ld_rec(rec2 + src(j)))], 1);
     __syncthreads();
     if (w == 0) {  // cell starts; zrun becomes each cell's running output position
         int carry = cs;
@@ -553,8 +572,9 @@ __device__ __forceinline__ void z_sort_chunked(const Geometry& g, int col, int c
             const int jl = w * (kZRounds * 32) + u * 32 + lane;
             zr[u] = -1 - lane;
             if (jl < cm) {
-                v[u] = ld_rec(rec2 + cs + c0 + jl);
-                ir[u] = __ldg(idx2 + cs + c0 + jl);
+                const int64_t sj = src(c0 + jl);
+                v[u] = ld_rec(rec2 + sj);
+                ir[u] = __ldg(idx2 + sj);
                 zr[u] = rec_c2(g, v[u]);
             }
         }
@@ -643,7 +663,259 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_sort(Geometry g,
     if (ZB <= 6 && whole_ok && m <= kZCap)  // uniform per CTA
         z_sort_whole<(ZB <= 6 ? ZB : 6)>(g, col, cs, m, n, idx2, rec2, perm, start, sp, zsm, &zbar, wsum);
     else
-        z_sort_chunked<ZB>(g, col, cs, m, n, idx2, rec2, perm, start, sp, zsm);
+        z_sort_chunked<ZB>(g, col, cs, m, ContiguousSrc{cs}, n, idx2, rec2, perm, start, sp, zsm);
+}
+
+// ---- tile-sorted variant (the default where it fits) ----------------------
+// k_tile_sort   one CTA per tile of kTile particles: cell keys, box checks and a
+//               stable tile-local counting sort by column in shared memory; the
+//               tile leaves column-ordered as one contiguous run, with its
+//               column offsets toff[tile][0..ncol] and column totals added to
+//               ctot (integer atomics: order-free, so deterministic)
+// k_z_tiles     one CTA per column: column base from ctot, the column's piece
+//               of every tile gathered in ascending tile order (= ascending
+//               particle order), then the whole-column z sort above
+// This replaces k_tile_hist + k_col_scan + k_col_scatter: no cross-tile scan,
+// and no scattered 32-byte record stores (scripts/probes/scatter_probe.cu).
+struct TileLayout {
+    size_t rec, idx, wc, tc, cb, total;
+    __host__ __device__ explicit TileLayout(int ncol) {
+        rec = 0;
+        idx = rec + sizeof(double4) * kTile;
+        wc = idx + sizeof(int32_t) * kTile;
+        tc = wc + ((sizeof(uint16_t) * kTileWarps * ncol + 15) & ~size_t(15));
+        cb = tc + sizeof(int32_t) * ncol;
+        total = cb + sizeof(int32_t) * (ncol + 1);
+    }
+};
+constexpr size_t kTileMaxSmem = 200 * 1024;
+
+template <int CB>
+__global__ void __launch_bounds__(kTileWarps * 32, 2) k_tile_sort(Geometry g, int64_t n,
+                                                               const double* __restrict__ xyz,
+                                                               const double* __restrict__ q,
+                                                               int32_t* __restrict__ toff,
+                                                               int32_t* __restrict__ ctot,
+                                                               int32_t* __restrict__ idx2,
+                                                               double4* __restrict__ rec2,
+                                                               unsigned long long* bad) {
+    extern __shared__ __align__(16) unsigned char tsm[];
+    __shared__ int32_t wsum[32];
+    const int ncol = g.K[0] * g.K[1];
+    const TileLayout TL(ncol);
+    double4* s_rec = reinterpret_cast<double4*>(tsm + TL.rec);
+    int32_t* s_idx = reinterpret_cast<int32_t*>(tsm + TL.idx);
+    uint16_t* wc = reinterpret_cast<uint16_t*>(tsm + TL.wc);  // [kTileWarps][ncol]
+    int32_t* tc = reinterpret_cast<int32_t*>(tsm + TL.tc);    // [ncol] tile column counts
+    int32_t* cb = reinterpret_cast<int32_t*>(tsm + TL.cb);    // [ncol + 1] tile column starts
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    for (int e = tid; e < kTileWarps * ncol; e += blockDim.x) wc[e] = 0;
+    const int64_t tbase = (int64_t)blockIdx.x * kTile;
+    const int64_t wbase = tbase + w * (kRounds * 32);
+    double4 rv[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {  // every load of the warp's slice in flight
+        const int64_t i = wbase + r * 32 + lane;
+        if (i < n)
+            rv[r] = make_double4(__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2),
+                                 q ? __ldg(q + i) : 0.0);
+    }
+    const double b = __dmul_rn(2.0, g.radius), y = g.inv_diam;
+    int colr[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t i = wbase + r * 32 + lane;
+        colr[r] = -1;
+        if (i < n) {
+            const double p0 = rv[r].x, p1 = rv[r].y, p2 = rv[r].z;
+            if (fabs(p0 - g.center[0]) > g.radius || fabs(p1 - g.center[1]) > g.radius ||
+                fabs(p2 - g.center[2]) > g.radius)
+                atomicMin(&bad[0], (unsigned long long)i);  // Box3::contains (geometry.hpp:36-40)
+            const int c0 = axis_cell2(p0, g.center[0], g.radius, g.K[0], b, y);
+            const int c1 = axis_cell2(p1, g.center[1], g.radius, g.K[1], b, y);
+            const int c2 = axis_cell2(p2, g.center[2], g.radius, g.K[2], b, y);
+            if (c0 < g.x_lo || c0 >= g.x_hi || c1 < g.y_lo || c1 >= g.y_hi || c2 < g.z_lo || c2 >= g.z_hi)
+                atomicOr(&bad[1], 2ull);  // not in this plan's cell block
+            colr[r] = c0 * g.K[1] + c1;
+        }
+    }
+    __syncthreads();
+    // 1: per-warp column counts (peer masks kept for the placement)
+    unsigned pk[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const bool act = colr[r] >= 0;
+        const int col = act ? colr[r] : -1 - lane;
+        const unsigned peers = warp_peers<CB>(col);
+        pk[r] = peers;
+        if (act && lane == __ffs(peers) - 1) wc[w * ncol + col] += (uint16_t)__popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // 2: exclusive over warps inside each column, column totals, then the
+    // exclusive scan over columns: the tile's column-ordered layout
+    for (int c = tid; c < ncol; c += blockDim.x) {
+        int run = 0;
+#pragma unroll
+        for (int k = 0; k < kTileWarps; ++k) {
+            const int t = wc[k * ncol + c];
+            wc[k * ncol + c] = (uint16_t)run;
+            run += t;
+        }
+        tc[c] = run;
+    }
+    __syncthreads();
+    block_col_bases(tc, ncol, cb, wsum);
+    int32_t* trow = toff + (int64_t)blockIdx.x * (ncol + 1);
+    for (int c = tid; c <= ncol; c += blockDim.x) trow[c] = cb[c];
+    for (int c = tid; c < ncol; c += blockDim.x)
+        if (tc[c]) atomicAdd(&ctot[c], tc[c]);
+    // 3: placement in index order into the staged tile
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const bool act = colr[r] >= 0;
+        const unsigned peers = pk[r];
+        int base = 0;
+        if (act) base = cb[colr[r]] + wc[w * ncol + colr[r]];
+        __syncwarp();
+        if (act) {
+            if (lane == __ffs(peers) - 1) wc[w * ncol + colr[r]] += (uint16_t)__popc(peers);
+            const int pos = base + __popc(peers & ((1u << lane) - 1));
+            s_rec[pos] = rv[r];
+            s_idx[pos] = (int32_t)(wbase + r * 32 + lane);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    // 4: the tile leaves as one contiguous run
+    const int tn = cb[ncol];
+    for (int k = tid; k < tn; k += blockDim.x) {
+        st_rec(rec2 + tbase + k, s_rec[k]);
+        idx2[tbase + k] = s_idx[k];
+    }
+}
+
+__device__ __forceinline__ void cp_async16_s(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4_s(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// The column's piece tables: pre[t] = column-local start of tile t's piece
+// (pre[ntiles] = m), srca[t] = the piece's position in rec2/idx2.
+struct PieceSrc {
+    const int32_t* pre;
+    const int32_t* srca;
+    int ntiles;
+    __device__ int64_t operator()(int j) const {
+        int lo = 0, hi = ntiles;  // largest t with pre[t] <= j
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pre[mid] <= j) lo = mid; else hi = mid;
+        }
+        return (int64_t)srca[lo] + (j - pre[lo]);
+    }
+};
+
+// Shared-memory plan of k_z_tiles (host and device agree on it).
+struct ZTilesLayout {
+    size_t tables, total_whole, total_chunked;
+    __host__ __device__ ZTilesLayout(int K2, int ntiles) {
+        const size_t tb = sizeof(int32_t) * (2 * (size_t)ntiles + 1);
+        const ZWholeLayout W(K2);
+        // whole path: the tables alias the z counters (zeroed after staging)
+        tables = W.cnt;
+        total_whole = W.cnt + ((tb > W.total - W.cnt) ? tb : W.total - W.cnt);
+        total_chunked = ZLayout(K2).total + tb;
+    }
+};
+
+template <int ZB>
+__global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n, int ntiles,
+                                                        int whole_ok,
+                                                        const int32_t* __restrict__ ctot,
+                                                        const int32_t* __restrict__ toff,
+                                                        const int32_t* __restrict__ idx2,
+                                                        const double4* __restrict__ rec2,
+                                                        int32_t* __restrict__ perm,
+                                                        int32_t* __restrict__ start,
+                                                        double4* __restrict__ sp) {
+    extern __shared__ __align__(16) unsigned char zsm[];
+    __shared__ int32_t wsum[32];
+    const int col = blockIdx.x, ncol = g.K[0] * g.K[1], K2 = g.K[2];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int m = __ldg(ctot + col);
+    const bool whole = ZB <= 6 && whole_ok && m <= kZCap;  // uniform per CTA
+    const ZTilesLayout TL(K2, ntiles);
+    int32_t* pre = reinterpret_cast<int32_t*>(zsm + (whole ? TL.tables : ZLayout(K2).total));
+    int32_t* srca = pre + ntiles + 1;
+    // column base cs = sum of the earlier columns' totals; the piece of every
+    // tile (thread-contiguous slices of tiles, so the scan is in tile order)
+    const int per = (ntiles + kZThreads - 1) / kZThreads;
+    const int lo = min(ntiles, tid * per), hi = min(ntiles, lo + per);
+    int csum = 0;
+    for (int c = tid; c < col; c += kZThreads) csum += __ldg(ctot + c);
+    int psum = 0;
+    for (int t = lo; t < hi; ++t) {
+        const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
+        const int e = __ldg(toff + (int64_t)t * (ncol + 1) + col + 1);
+        srca[t] = t * kTile + a;
+        pre[t] = e - a;  // count for now
+        psum += e - a;
+    }
+    int x = psum, cx = csum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y1 = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y1;
+        cx += __shfl_xor_sync(0xffffffffu, cx, o);
+    }
+    if (lane == 31) wsum[w] = x;
+    if (lane == 0) wsum[16 + w] = cx;
+    __syncthreads();
+    int off = 0, cs = 0;
+    for (int k = 0; k < kZWarps; ++k) {
+        off += k < w ? wsum[k] : 0;
+        cs += wsum[16 + k];
+    }
+    int run = off + x - psum;
+    for (int t = lo; t < hi; ++t) {
+        const int c = pre[t];
+        pre[t] = run;
+        run += c;
+    }
+    if (tid == 0) pre[ntiles] = m;
+    __syncthreads();
+    if (!whole) {
+        z_sort_chunked<ZB>(g, col, cs, m, PieceSrc{pre, srca, ntiles}, n, idx2, rec2, perm, start, sp,
+                           zsm);
+        return;
+    }
+    const ZWholeLayout L(K2);
+    double4* s_rec = reinterpret_cast<double4*>(zsm + L.rec);
+    int32_t* s_idx = reinterpret_cast<int32_t*>(zsm + L.idx);
+    uint16_t* s_inv = reinterpret_cast<uint16_t*>(zsm + L.inv);  // piece owner of each element first
+    uint8_t* s_z = reinterpret_cast<uint8_t*>(zsm + L.z);
+    uint16_t* cnt = reinterpret_cast<uint16_t*>(zsm + L.cnt);
+    for (int t = lo; t < hi; ++t)
+        for (int j = pre[t]; j < pre[t + 1]; ++j) s_inv[j] = (uint16_t)t;
+    __syncthreads();
+    for (int j = tid; j < m; j += kZThreads) {
+        const int t = s_inv[j];
+        const int64_t src = (int64_t)srca[t] + (j - pre[t]);
+        cp_async16_s(s_rec + j, rec2 + src);
+        cp_async16_s(reinterpret_cast<char*>(s_rec + j) + 16, reinterpret_cast<const char*>(rec2 + src) + 16);
+        cp_async4_s(s_idx + j, idx2 + src);
+    }
+    cp_async_wait_all();
+    __syncthreads();  // staged; the tables (aliasing cnt) are no longer read
+    for (int e = tid; e < K2 * kZThreads; e += kZThreads) cnt[e] = 0;
+    __syncthreads();
+    z_whole_body<(ZB <= 6 ? ZB : 6)>(g, col, cs, m, n, s_rec, s_idx, s_inv, s_z, cnt, perm, start, sp,
+                                     wsum);
 }
 
 // Instantiation for an even key width in [2, 16].
@@ -669,14 +941,70 @@ bool sort2_supported(const Geometry& g) {
            ZLayout(g.K[2]).total <= 160 * 1024 && g.K[2] <= 65536;
 }
 
-size_t sort2_hist_entries(const Geometry& g, int64_t cap) {
+size_t sort2_hist_entries(const Geometry& g, int64_t cap) {  // also the tile path's toff
     const int64_t ntiles = (cap + kTile - 1) / kTile;
-    return (size_t)g.K[0] * g.K[1] * (size_t)std::max<int64_t>(1, ntiles);
+    return ((size_t)g.K[0] * g.K[1] + 1) * (size_t)std::max<int64_t>(1, ntiles);
+}
+
+// Variant choice. The tile path wins while a tile's piece of a column holds
+// several particles on average (config 2: 38.8 -> 29.3 us); with ~5 (config 3)
+// it ties the column scatter (67.7 vs 70.2 us), and with ~1 (config 4) the
+// per-tile column tables dominate (308 vs 234 us). KPME_SORT_TILES=0 / 1
+// forces the column scatter / the tile path wherever it fits (tests, A/B).
+static bool tiles_chosen(int ncol) {
+    static int m = -1;
+    if (m < 0) {
+        const char* e = getenv("KPME_SORT_TILES");
+        m = (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 1 : 2;
+    }
+    return m == 1 || (m == 2 && ncol * 8 <= kTile);
+}
+
+static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, const SortBuffers& b,
+                               cudaStream_t s, int* launches, const double* q, double4* sp) {
+    const int ncol = g.K[0] * g.K[1];
+    const int ntiles = (int)std::max<int64_t>(1, (n + kTile - 1) / kTile);
+    const TileLayout TL(ncol);
+    const ZTilesLayout ZL(g.K[2], ntiles);
+    if (!tiles_chosen(ncol) || TL.total > kTileMaxSmem || ntiles > 65535 || ZL.total_chunked > 160 * 1024)
+        return false;
+    const int cb = (bits_for(ncol) + 1) & ~1, zb = (bits_for(g.K[2]) + 1) & ~1;
+    static bool attr = false;
+    if (!attr) {
+        for (int bb = 2; bb <= 16; bb += 2) {
+            KB_CUDA(cudaFuncSetAttribute(pick_bits(bb, [](auto B) { return &k_tile_sort<decltype(B)::value>; }),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileMaxSmem));
+            KB_CUDA(cudaFuncSetAttribute(pick_bits(bb, [](auto B) { return &k_z_tiles<decltype(B)::value>; }),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        }
+        attr = true;
+    }
+    auto tile_kernel = pick_bits(cb, [](auto B) { return &k_tile_sort<decltype(B)::value>; });
+    auto z_kernel = pick_bits(zb, [](auto B) { return &k_z_tiles<decltype(B)::value>; });
+    KB_CUDA(cudaMemsetAsync(b.ctot, 0, sizeof(int32_t) * ncol, s));
+    int l = 0;
+    if (n > 0) {
+        tile_kernel<<<ntiles, kTileWarps * 32, TL.total, s>>>(g, n, xyz, q, b.hist, b.ctot, b.idx2, b.rec,
+                                                             b.bad);
+        KB_CHECK_LAUNCH();
+        ++l;
+    } else {
+        KB_CUDA(cudaMemsetAsync(b.hist, 0, sizeof(int32_t) * (ncol + 1), s));
+    }
+    const int whole_ok = ZL.total_whole <= kZWholeMaxSmem && g.K[2] <= 64;
+    const size_t zsmem = std::max(ZL.total_chunked, whole_ok ? ZL.total_whole : 0);
+    z_kernel<<<ncol, kZThreads, zsmem, s>>>(g, n, ntiles, whole_ok, b.ctot, b.hist, b.idx2, b.rec, b.perm,
+                                            b.start, sp);
+    KB_CHECK_LAUNCH();
+    ++l;
+    if (launches) *launches += l;
+    return true;
 }
 
 void launch_sort2(const Geometry& g, int64_t n, const double* xyz, const SortBuffers& b,
                   cudaStream_t s, int* launches, const double* q, double4* sp) {
     if (!q) sp = nullptr;
+    if (launch_sort2_tiles(g, n, xyz, b, s, launches, q, sp)) return;
     // key widths rounded up to an even bit count (extra ballots see zero bits)
     const int ncol = g.K[0] * g.K[1];
     const int cb = (bits_for(ncol) + 1) & ~1, zb = (bits_for(g.K[2]) + 1) & ~1;

@@ -498,3 +498,24 @@ def test_e2e_clustered_cells(oracle, order):
     plan = plan_for(pb)
     z = plan.execute(dev(pb.pos), dev(pb.q)).cpu().numpy()
     assert rel(z, oracle.kpme_apply(pb)) <= E2E_TOL
+
+
+@pytest.mark.parametrize("variant", ["0", "1"])
+def test_sort_variants_forced(variant):
+    """Both cell-sort variants of sort2.cu (column scatter, tile sort), forced
+    for every shape where they fit (the default picks per shape): the
+    bit-exact sort tests, the clustered columns above the whole-column
+    capacity (the tile path's chunked piece gather) and end to end at
+    configs 2 and 3. The variant is read once per process, hence the
+    subprocess."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KPME_SORT_TILES=variant)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
+                        "tests/test_gpu_parity.py", "-k",
+                        "(sort and not variants) or clustered or cfg2_vs or cfg3_vs or chunk"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout

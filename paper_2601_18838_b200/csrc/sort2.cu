@@ -350,17 +350,25 @@ constexpr int kZCap = 2560;  // <= 10 particles per thread (4-bit counters)
 constexpr int kZThreads = kZWarps * 32;
 struct ZWholeLayout {
     size_t rec, idx, inv, z, cnt, total;
-    __host__ __device__ explicit ZWholeLayout(int K2) {
+    __host__ __device__ ZWholeLayout(int K2, int cap) {
         rec = 0;
-        idx = sizeof(double4) * kZCap;
-        inv = idx + sizeof(int32_t) * (kZCap + 4);
-        z = inv + sizeof(uint16_t) * kZCap;
-        cnt = z + sizeof(uint8_t) * kZCap;
+        idx = sizeof(double4) * cap;
+        inv = idx + sizeof(int32_t) * (cap + 4);
+        z = inv + sizeof(uint16_t) * cap;
+        cnt = z + sizeof(uint8_t) * cap;
         cnt = (cnt + 15) & ~size_t(15);
         total = cnt + sizeof(uint16_t) * (size_t)K2 * kZThreads;
     }
 };
 constexpr size_t kZWholeMaxSmem = 112 * 1024;  // two CTAs per SM
+// Largest whole-column capacity whose layout keeps two CTAs per SM (the z
+// counters grow with K2: config 4's 43 cells per column fit 2048); 0: none.
+__host__ inline int whole_cap_for(int K2) {
+    if (K2 > 64) return 0;
+    for (int cap = kZCap; cap >= 1024; cap -= 512)
+        if (ZWholeLayout(K2, cap).total <= kZWholeMaxSmem) return cap;
+    return 0;
+}
 
 // Steps 2-5 of the whole-column sort: the column's m records and indices are
 // staged in shared memory in ascending particle order and cnt is zeroed.
@@ -472,9 +480,9 @@ __device__ __forceinline__ void z_sort_whole(const Geometry& g, int col, int cs,
                                              int32_t* __restrict__ perm,
                                              int32_t* __restrict__ start,
                                              double4* __restrict__ sp, unsigned char* zsm,
-                                             uint64_t* bar, int32_t* wsum) {
+                                             uint64_t* bar, int32_t* wsum, int cap) {
     const int K2 = g.K[2];
-    const ZWholeLayout L(K2);
+    const ZWholeLayout L(K2, cap);
     double4* s_rec = reinterpret_cast<double4*>(zsm + L.rec);
     int32_t* s_idx = reinterpret_cast<int32_t*>(zsm + L.idx);
     uint16_t* s_inv = reinterpret_cast<uint16_t*>(zsm + L.inv);
@@ -649,7 +657,7 @@ __device__ __forceinline__ void z_sort_chunked(const Geometry& g, int col, int c
 template <int ZB>
 __global__ void __launch_bounds__(kZThreads, 2) k_z_sort(Geometry g,
                                                        const int32_t* __restrict__ cbase,
-                                                       int64_t n, int whole_ok,
+                                                       int64_t n, int whole_cap,
                                                        const int32_t* __restrict__ idx2,
                                                        const double4* __restrict__ rec2,
                                                        int32_t* __restrict__ perm,
@@ -660,8 +668,9 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_sort(Geometry g,
     __shared__ uint64_t zbar;
     const int col = blockIdx.x;
     const int cs = __ldg(cbase + col), m = __ldg(cbase + col + 1) - cs;
-    if (ZB <= 6 && whole_ok && m <= kZCap)  // uniform per CTA
-        z_sort_whole<(ZB <= 6 ? ZB : 6)>(g, col, cs, m, n, idx2, rec2, perm, start, sp, zsm, &zbar, wsum);
+    if (ZB <= 6 && m <= whole_cap)  // uniform per CTA
+        z_sort_whole<(ZB <= 6 ? ZB : 6)>(g, col, cs, m, n, idx2, rec2, perm, start, sp, zsm, &zbar, wsum,
+                                         whole_cap);
     else
         z_sort_chunked<ZB>(g, col, cs, m, ContiguousSrc{cs}, n, idx2, rec2, perm, start, sp, zsm);
 }
@@ -824,9 +833,9 @@ struct PieceSrc {
 // Shared-memory plan of k_z_tiles (host and device agree on it).
 struct ZTilesLayout {
     size_t tables, total_whole, total_chunked;
-    __host__ __device__ ZTilesLayout(int K2, int ntiles) {
+    __host__ __device__ ZTilesLayout(int K2, int ntiles, int cap) {
         const size_t tb = sizeof(int32_t) * (2 * (size_t)ntiles + 1);
-        const ZWholeLayout W(K2);
+        const ZWholeLayout W(K2, cap > 0 ? cap : kZCap);
         // whole path: the tables alias the z counters (zeroed after staging)
         tables = W.cnt;
         total_whole = W.cnt + ((tb > W.total - W.cnt) ? tb : W.total - W.cnt);
@@ -836,7 +845,7 @@ struct ZTilesLayout {
 
 template <int ZB>
 __global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n, int ntiles,
-                                                        int whole_ok,
+                                                        int whole_cap,
                                                         const int32_t* __restrict__ ctot,
                                                         const int32_t* __restrict__ toff,
                                                         const int32_t* __restrict__ idx2,
@@ -849,8 +858,8 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n,
     const int col = blockIdx.x, ncol = g.K[0] * g.K[1], K2 = g.K[2];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int m = __ldg(ctot + col);
-    const bool whole = ZB <= 6 && whole_ok && m <= kZCap;  // uniform per CTA
-    const ZTilesLayout TL(K2, ntiles);
+    const bool whole = ZB <= 6 && m <= whole_cap;  // uniform per CTA
+    const ZTilesLayout TL(K2, ntiles, whole_cap);
     int32_t* pre = reinterpret_cast<int32_t*>(zsm + (whole ? TL.tables : ZLayout(K2).total));
     int32_t* srca = pre + ntiles + 1;
     // column base cs = sum of the earlier columns' totals; the piece of every
@@ -894,7 +903,7 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n,
                            zsm);
         return;
     }
-    const ZWholeLayout L(K2);
+    const ZWholeLayout L(K2, whole_cap);
     double4* s_rec = reinterpret_cast<double4*>(zsm + L.rec);
     int32_t* s_idx = reinterpret_cast<int32_t*>(zsm + L.idx);
     uint16_t* s_inv = reinterpret_cast<uint16_t*>(zsm + L.inv);  // piece owner of each element first
@@ -965,7 +974,8 @@ static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, 
     const int ncol = g.K[0] * g.K[1];
     const int ntiles = (int)std::max<int64_t>(1, (n + kTile - 1) / kTile);
     const TileLayout TL(ncol);
-    const ZTilesLayout ZL(g.K[2], ntiles);
+    const int wcap = whole_cap_for(g.K[2]);
+    const ZTilesLayout ZL(g.K[2], ntiles, wcap);
     if (!tiles_chosen(ncol) || TL.total > kTileMaxSmem || ntiles > 65535 || ZL.total_chunked > 160 * 1024)
         return false;
     const int cb = (bits_for(ncol) + 1) & ~1, zb = (bits_for(g.K[2]) + 1) & ~1;
@@ -991,9 +1001,10 @@ static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, 
     } else {
         KB_CUDA(cudaMemsetAsync(b.hist, 0, sizeof(int32_t) * (ncol + 1), s));
     }
-    const int whole_ok = ZL.total_whole <= kZWholeMaxSmem && g.K[2] <= 64;
-    const size_t zsmem = std::max(ZL.total_chunked, whole_ok ? ZL.total_whole : 0);
-    z_kernel<<<ncol, kZThreads, zsmem, s>>>(g, n, ntiles, whole_ok, b.ctot, b.hist, b.idx2, b.rec, b.perm,
+    // the piece tables alias the z counters only when they fit there
+    const int whole_cap = wcap > 0 && ZL.total_whole <= kZWholeMaxSmem ? wcap : 0;
+    const size_t zsmem = std::max(ZL.total_chunked, whole_cap ? ZL.total_whole : 0);
+    z_kernel<<<ncol, kZThreads, zsmem, s>>>(g, n, ntiles, whole_cap, b.ctot, b.hist, b.idx2, b.rec, b.perm,
                                             b.start, sp);
     KB_CHECK_LAUNCH();
     ++l;
@@ -1042,10 +1053,10 @@ void launch_sort2(const Geometry& g, int64_t n, const double* xyz, const SortBuf
         KB_CHECK_LAUNCH();
         ++l;
     }
-    const size_t wsmem = ZWholeLayout(g.K[2]).total;
-    const int whole_ok = wsmem <= kZWholeMaxSmem && g.K[2] <= 64;
-    const size_t zsmem = std::max(ZLayout(g.K[2]).total, whole_ok ? wsmem : 0);
-    z_kernel<<<ncol, kZThreads, zsmem, s>>>(g, b.cbase, n, whole_ok, b.idx2, b.rec, b.perm,
+    const int whole_cap = whole_cap_for(g.K[2]);
+    const size_t zsmem = std::max(ZLayout(g.K[2]).total,
+                                  whole_cap ? ZWholeLayout(g.K[2], whole_cap).total : 0);
+    z_kernel<<<ncol, kZThreads, zsmem, s>>>(g, b.cbase, n, whole_cap, b.idx2, b.rec, b.perm,
                                             b.start, sp);
     KB_CHECK_LAUNCH();
     ++l;

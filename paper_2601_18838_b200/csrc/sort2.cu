@@ -679,11 +679,12 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_sort(Geometry g,
 // k_tile_sort   one CTA per tile of kTile particles: cell keys, box checks and a
 //               stable tile-local counting sort by column in shared memory; the
 //               tile leaves column-ordered as one contiguous run, with its
-//               column offsets toff[tile][0..ncol] and column totals added to
-//               ctot (integer atomics: order-free, so deterministic)
-// k_z_tiles     one CTA per column: column base from ctot, the column's piece
-//               of every tile gathered in ascending tile order (= ascending
-//               particle order), then the whole-column z sort above
+//               column offsets toff[tile][0..ncol]
+// k_z_tiles     one CTA per column: the column's piece of every tile gathered
+//               in ascending tile order (= ascending particle order), then the
+//               whole-column z sort above. Its base is sum_t toff[t][col]: a
+//               tile's offset of the column counts exactly the tile's particles
+//               of the earlier columns.
 // This replaces k_tile_hist + k_col_scan + k_col_scatter: no cross-tile scan,
 // and no scattered 32-byte record stores (scripts/probes/scatter_probe.cu).
 struct TileLayout {
@@ -704,7 +705,6 @@ __global__ void __launch_bounds__(kTileWarps * 32, 2) k_tile_sort(Geometry g, in
                                                                const double* __restrict__ xyz,
                                                                const double* __restrict__ q,
                                                                int32_t* __restrict__ toff,
-                                                               int32_t* __restrict__ ctot,
                                                                int32_t* __restrict__ idx2,
                                                                double4* __restrict__ rec2,
                                                                unsigned long long* bad) {
@@ -718,7 +718,8 @@ __global__ void __launch_bounds__(kTileWarps * 32, 2) k_tile_sort(Geometry g, in
     int32_t* tc = reinterpret_cast<int32_t*>(tsm + TL.tc);    // [ncol] tile column counts
     int32_t* cb = reinterpret_cast<int32_t*>(tsm + TL.cb);    // [ncol + 1] tile column starts
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-    for (int e = tid; e < kTileWarps * ncol; e += blockDim.x) wc[e] = 0;
+    for (int e = tid; e < (int)((TL.tc - TL.wc) / 16); e += blockDim.x)
+        reinterpret_cast<uint4*>(wc)[e] = make_uint4(0u, 0u, 0u, 0u);
     const int64_t tbase = (int64_t)blockIdx.x * kTile;
     const int64_t wbase = tbase + w * (kRounds * 32);
     double4 rv[kRounds];
@@ -777,8 +778,6 @@ __global__ void __launch_bounds__(kTileWarps * 32, 2) k_tile_sort(Geometry g, in
     block_col_bases(tc, ncol, cb, wsum);
     int32_t* trow = toff + (int64_t)blockIdx.x * (ncol + 1);
     for (int c = tid; c <= ncol; c += blockDim.x) trow[c] = cb[c];
-    for (int c = tid; c < ncol; c += blockDim.x)
-        if (tc[c]) atomicAdd(&ctot[c], tc[c]);
     // 3: placement in index order into the staged tile
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
@@ -846,7 +845,6 @@ struct ZTilesLayout {
 template <int ZB>
 __global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n, int ntiles,
                                                         int whole_cap,
-                                                        const int32_t* __restrict__ ctot,
                                                         const int32_t* __restrict__ toff,
                                                         const int32_t* __restrict__ idx2,
                                                         const double4* __restrict__ rec2,
@@ -857,24 +855,33 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n,
     __shared__ int32_t wsum[32];
     const int col = blockIdx.x, ncol = g.K[0] * g.K[1], K2 = g.K[2];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int m = __ldg(ctot + col);
-    const bool whole = ZB <= 6 && m <= whole_cap;  // uniform per CTA
-    const ZTilesLayout TL(K2, ntiles, whole_cap);
-    int32_t* pre = reinterpret_cast<int32_t*>(zsm + (whole ? TL.tables : ZLayout(K2).total));
-    int32_t* srca = pre + ntiles + 1;
-    // column base cs = sum of the earlier columns' totals; the piece of every
-    // tile (thread-contiguous slices of tiles, so the scan is in tile order)
+    // the piece of every tile (thread-contiguous slices of tiles, so the scan
+    // is in tile order) into the tables past the chunked layout; the whole
+    // path's (aliasing its z counters) gets them copied once m is known
     const int per = (ntiles + kZThreads - 1) / kZThreads;
     const int lo = min(ntiles, tid * per), hi = min(ntiles, lo + per);
-    int csum = 0;
-    for (int c = tid; c < col; c += kZThreads) csum += __ldg(ctot + c);
-    int psum = 0;
-    for (int t = lo; t < hi; ++t) {
-        const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
-        const int e = __ldg(toff + (int64_t)t * (ncol + 1) + col + 1);
-        srca[t] = t * kTile + a;
-        pre[t] = e - a;  // count for now
-        psum += e - a;
+    const ZTilesLayout TL(K2, ntiles, whole_cap);
+    int a_[4], e_[4];
+    int csum = 0, psum = 0;
+    if (per <= 4) {  // loads in flight together (every shape the tile path takes)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (lo + u < hi) {
+                a_[u] = __ldg(toff + (int64_t)(lo + u) * (ncol + 1) + col);
+                e_[u] = __ldg(toff + (int64_t)(lo + u) * (ncol + 1) + col + 1);
+            }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (lo + u < hi) {
+                csum += a_[u];
+                psum += e_[u] - a_[u];
+            }
+    } else {
+        for (int t = lo; t < hi; ++t) {
+            const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
+            csum += a;
+            psum += __ldg(toff + (int64_t)t * (ncol + 1) + col + 1) - a;
+        }
     }
     int x = psum, cx = csum;
     for (int o = 1; o < 32; o <<= 1) {
@@ -890,14 +897,31 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n,
         off += k < w ? wsum[k] : 0;
         cs += wsum[16 + k];
     }
+    int m = 0;
+    for (int k = 0; k < kZWarps; ++k) m += wsum[k];
+    const bool whole = ZB <= 6 && m <= whole_cap;  // uniform per CTA
+    int32_t* pre = reinterpret_cast<int32_t*>(zsm + (whole ? TL.tables : ZLayout(K2).total));
+    int32_t* srca = pre + ntiles + 1;
     int run = off + x - psum;
-    for (int t = lo; t < hi; ++t) {
-        const int c = pre[t];
-        pre[t] = run;
-        run += c;
+    if (per <= 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (lo + u < hi) {
+                srca[lo + u] = (lo + u) * kTile + a_[u];
+                pre[lo + u] = run;
+                run += e_[u] - a_[u];
+            }
+    } else {
+        for (int t = lo; t < hi; ++t) {
+            const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
+            srca[t] = t * kTile + a;
+            pre[t] = run;
+            run += __ldg(toff + (int64_t)t * (ncol + 1) + col + 1) - a;
+        }
     }
     if (tid == 0) pre[ntiles] = m;
     __syncthreads();
+
     if (!whole) {
         z_sort_chunked<ZB>(g, col, cs, m, PieceSrc{pre, srca, ntiles}, n, idx2, rec2, perm, start, sp,
                            zsm);
@@ -956,17 +980,17 @@ size_t sort2_hist_entries(const Geometry& g, int64_t cap) {  // also the tile pa
 }
 
 // Variant choice. The tile path wins while a tile's piece of a column holds
-// several particles on average (config 2: 38.8 -> 29.3 us); with ~5 (config 3)
-// it ties the column scatter (67.7 vs 70.2 us), and with ~1 (config 4) the
-// per-tile column tables dominate (308 vs 234 us). KPME_SORT_TILES=0 / 1
-// forces the column scatter / the tile path wherever it fits (tests, A/B).
+// a few particles on average (config 2, ~17: 38.3 -> 28.4 us; config 3, ~5:
+// 70.1 -> 64.1 us); with ~1 (config 4) the per-tile column tables dominate
+// (308 vs 234 us). KPME_SORT_TILES=0 / 1 forces the column scatter / the tile
+// path wherever it fits (tests, A/B).
 static bool tiles_chosen(int ncol) {
     static int m = -1;
     if (m < 0) {
         const char* e = getenv("KPME_SORT_TILES");
         m = (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 1 : 2;
     }
-    return m == 1 || (m == 2 && ncol * 8 <= kTile);
+    return m == 1 || (m == 2 && ncol * 4 <= kTile);
 }
 
 static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, const SortBuffers& b,
@@ -991,11 +1015,9 @@ static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, 
     }
     auto tile_kernel = pick_bits(cb, [](auto B) { return &k_tile_sort<decltype(B)::value>; });
     auto z_kernel = pick_bits(zb, [](auto B) { return &k_z_tiles<decltype(B)::value>; });
-    KB_CUDA(cudaMemsetAsync(b.ctot, 0, sizeof(int32_t) * ncol, s));
     int l = 0;
     if (n > 0) {
-        tile_kernel<<<ntiles, kTileWarps * 32, TL.total, s>>>(g, n, xyz, q, b.hist, b.ctot, b.idx2, b.rec,
-                                                             b.bad);
+        tile_kernel<<<ntiles, kTileWarps * 32, TL.total, s>>>(g, n, xyz, q, b.hist, b.idx2, b.rec, b.bad);
         KB_CHECK_LAUNCH();
         ++l;
     } else {
@@ -1004,7 +1026,7 @@ static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, 
     // the piece tables alias the z counters only when they fit there
     const int whole_cap = wcap > 0 && ZL.total_whole <= kZWholeMaxSmem ? wcap : 0;
     const size_t zsmem = std::max(ZL.total_chunked, whole_cap ? ZL.total_whole : 0);
-    z_kernel<<<ncol, kZThreads, zsmem, s>>>(g, n, ntiles, whole_cap, b.ctot, b.hist, b.idx2, b.rec, b.perm,
+    z_kernel<<<ncol, kZThreads, zsmem, s>>>(g, n, ntiles, whole_cap, b.hist, b.idx2, b.rec, b.perm,
                                             b.start, sp);
     KB_CHECK_LAUNCH();
     ++l;

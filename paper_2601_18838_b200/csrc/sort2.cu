@@ -834,11 +834,10 @@ struct ZTilesLayout {
     size_t tables, total_whole, total_chunked;
     __host__ __device__ ZTilesLayout(int K2, int ntiles, int cap) {
         const size_t tb = sizeof(int32_t) * (2 * (size_t)ntiles + 1);
-        const ZWholeLayout W(K2, cap > 0 ? cap : kZCap);
-        // whole path: the tables alias the z counters (zeroed after staging)
-        tables = W.cnt;
-        total_whole = W.cnt + ((tb > W.total - W.cnt) ? tb : W.total - W.cnt);
-        total_chunked = ZLayout(K2).total + tb;
+        // the whole path needs no tables (each thread stages its own pieces)
+        total_whole = cap > 0 ? ZWholeLayout(K2, cap).total : 0;
+        tables = ZLayout(K2).total;  // chunked path
+        total_chunked = tables + tb;
     }
 };
 
@@ -900,29 +899,18 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n,
     int m = 0;
     for (int k = 0; k < kZWarps; ++k) m += wsum[k];
     const bool whole = ZB <= 6 && m <= whole_cap;  // uniform per CTA
-    int32_t* pre = reinterpret_cast<int32_t*>(zsm + (whole ? TL.tables : ZLayout(K2).total));
-    int32_t* srca = pre + ntiles + 1;
     int run = off + x - psum;
-    if (per <= 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (lo + u < hi) {
-                srca[lo + u] = (lo + u) * kTile + a_[u];
-                pre[lo + u] = run;
-                run += e_[u] - a_[u];
-            }
-    } else {
+    if (!whole) {  // piece tables past the chunked layout, binary-searched per element
+        int32_t* pre = reinterpret_cast<int32_t*>(zsm + TL.tables);
+        int32_t* srca = pre + ntiles + 1;
         for (int t = lo; t < hi; ++t) {
             const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
             srca[t] = t * kTile + a;
             pre[t] = run;
             run += __ldg(toff + (int64_t)t * (ncol + 1) + col + 1) - a;
         }
-    }
-    if (tid == 0) pre[ntiles] = m;
-    __syncthreads();
-
-    if (!whole) {
+        if (tid == 0) pre[ntiles] = m;
+        __syncthreads();
         z_sort_chunked<ZB>(g, col, cs, m, PieceSrc{pre, srca, ntiles}, n, idx2, rec2, perm, start, sp,
                            zsm);
         return;
@@ -930,22 +918,37 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n,
     const ZWholeLayout L(K2, whole_cap);
     double4* s_rec = reinterpret_cast<double4*>(zsm + L.rec);
     int32_t* s_idx = reinterpret_cast<int32_t*>(zsm + L.idx);
-    uint16_t* s_inv = reinterpret_cast<uint16_t*>(zsm + L.inv);  // piece owner of each element first
+    uint16_t* s_inv = reinterpret_cast<uint16_t*>(zsm + L.inv);
     uint8_t* s_z = reinterpret_cast<uint8_t*>(zsm + L.z);
     uint16_t* cnt = reinterpret_cast<uint16_t*>(zsm + L.cnt);
-    for (int t = lo; t < hi; ++t)
-        for (int j = pre[t]; j < pre[t + 1]; ++j) s_inv[j] = (uint16_t)t;
+    // each thread writes the source positions of its own pieces into s_idx;
+    // the staging loop reads its element's slot before the cp.async that
+    // overwrites it with the particle index
+    if (per <= 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (lo + u < hi) {
+                const int c = e_[u] - a_[u], src0 = (lo + u) * kTile + a_[u];
+                for (int k = 0; k < c; ++k) s_idx[run + k] = src0 + k;
+                run += c;
+            }
+    } else {
+        for (int t = lo; t < hi; ++t) {
+            const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
+            const int c = __ldg(toff + (int64_t)t * (ncol + 1) + col + 1) - a, src0 = t * kTile + a;
+            for (int k = 0; k < c; ++k) s_idx[run + k] = src0 + k;
+            run += c;
+        }
+    }
+    for (int e = tid; e < K2 * kZThreads; e += kZThreads) cnt[e] = 0;
     __syncthreads();
     for (int j = tid; j < m; j += kZThreads) {
-        const int t = s_inv[j];
-        const int64_t src = (int64_t)srca[t] + (j - pre[t]);
+        const int src = s_idx[j];
         cp_async16_s(s_rec + j, rec2 + src);
         cp_async16_s(reinterpret_cast<char*>(s_rec + j) + 16, reinterpret_cast<const char*>(rec2 + src) + 16);
         cp_async4_s(s_idx + j, idx2 + src);
     }
     cp_async_wait_all();
-    __syncthreads();  // staged; the tables (aliasing cnt) are no longer read
-    for (int e = tid; e < K2 * kZThreads; e += kZThreads) cnt[e] = 0;
     __syncthreads();
     z_whole_body<(ZB <= 6 ? ZB : 6)>(g, col, cs, m, n, s_rec, s_idx, s_inv, s_z, cnt, perm, start, sp,
                                      wsum);

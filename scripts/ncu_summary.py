@@ -15,7 +15,8 @@ rows = list(csv.reader(io.StringIO(raw)))
 h, data = rows[0], rows[2:]
 KEYS = [("k_spread_uv", "k_spread_fwd"), ("k_spread_mma", "k_spread_fwd"), ("k_bwd_gather", "k_bwd_gather"),
         ("k_col_scatter", "k_col_scatter"), ("k_z_sort", "k_z_sort"), ("k_tile_hist", "k_tile_hist"),
-        ("k_col_scan", "k_col_scan"), ("k_core_sum", "k_core_sum")]
+        ("k_col_scan", "k_col_scan"), ("k_tile_sort", "k_tile_sort"), ("k_z_tiles", "k_z_tiles"),
+        ("k_core_sum", "k_core_sum")]
 M = {"time_us": "gpu__time_duration.sum", "dram_read": "dram__bytes_read.sum",
      "dram_write": "dram__bytes_write.sum", "inst": "smsp__inst_executed.sum",
      "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",

@@ -329,6 +329,8 @@ def run_ours(a):
         e2e_step()
     e2e_times = timed_steps(torch, e2e_step, a.steps, flush)
     e2e_ms = sum(e2e_times) / len(e2e_times)
+    e2e_sorted = sorted(e2e_times)
+    e2e_spread = {"min": e2e_sorted[0], "median": e2e_sorted[len(e2e_sorted) // 2], "max": e2e_sorted[-1]}
     if dist.is_initialized():
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -392,6 +394,7 @@ def run_ours(a):
                                    f"(NCCL core all-reduce)") if slab else "1 GPU",
                    "l2": "flushed (256 MiB write) before every timed step"},
         "e2e": {"value": w.n / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+                "ms_per_step_spread": e2e_spread,
                 "h2d_bytes_per_step": 32 * w.n, "d2h_bytes_per_step": 8 * w.n,
                 "path": ("SlabPlan.e2e_step: pinned H2D of the slab's particles, forward, "
                          "NCCL core all-reduce, backward, D2H" if slab else

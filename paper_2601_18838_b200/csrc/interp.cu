@@ -443,16 +443,29 @@ __device__ __forceinline__ void zero_padding(double* As, double* Bs, int lane) {
     for (int e = lane; e < (T::NT * 8 - T::L2) * T::LDP; e += 32) Bs[T::L2 * T::LDP + e] = 0.0;
 }
 
+// Fixed-order pairwise tree over red[0 .. 32 NW), run by the whole CTA (the
+// 128-thread tree for NW = 4); ends synchronised, result in red[0].
+template <int NW>
+__device__ __forceinline__ double block_tree_sum(double* red) {
+    constexpr int n = 32 * NW;
+    constexpr int top = n > 128 ? 128 : n > 64 ? 64 : n > 32 ? 32 : 16;
+    for (int o = top; o > 0; o >>= 1) {
+        if (threadIdx.x < o && threadIdx.x + o < n) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    return red[0];
+}
+
 // Column epilogue shared by the spread kernels: cross-warp sum of the warps'
 // T1 partials (at sm + w * per_warp + t1off, [L^2][RP]), then either the fused
 // y, x contractions into this column's partial core (Fpart) or the T1 slab.
 // epi: scratch for the contractions (spread_epilogue_doubles), not
 // overlapping any warp's T1 partial.
-template <int L>
+template <int L, int NW = 4>
 __device__ __forceinline__ void spread_epilogue(const ColumnArgs& a, const ColumnRange& cr, double* sm,
                                                 int per_warp, int t1off, int RP, double* epi,
                                                 double* red, double qsum, int want_fwd) {
-    constexpr int L2 = L * L, NW = 4;
+    constexpr int L2 = L * L, NT_ = 32 * NW;
     const Geometry& g = a.g;
     const int R = g.R;
     __syncthreads();
@@ -465,7 +478,7 @@ __device__ __forceinline__ void spread_epilogue(const ColumnArgs& a, const Colum
         double* tc = epi;  // [L^2][R]
         double* u = tc + L2 * R;            // [L][R][R]
         __syncthreads();
-        for (int e = threadIdx.x; e < L2 * R; e += 128) {
+        for (int e = threadIdx.x; e < L2 * R; e += NT_) {
             const int ij = e / R, r = e % R;
             double s = 0.0;
 #pragma unroll
@@ -474,12 +487,12 @@ __device__ __forceinline__ void spread_epilogue(const ColumnArgs& a, const Colum
         }
         __syncthreads();
         double* w01 = u + L * R * R;  // [2][R][L] the column's W0 / W1 rows
-        for (int e = threadIdx.x; e < R * L; e += 128) {
+        for (int e = threadIdx.x; e < R * L; e += NT_) {
             w01[e] = a.W0[(int64_t)(e / L) * g.n[0] + cr.c0 * L + e % L];
             w01[R * L + e] = a.W1[(int64_t)(e / L) * g.n[1] + cr.c1 * L + e % L];
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < L * R * R; e += 128) {
+        for (int e = threadIdx.x; e < L * R * R; e += NT_) {
             const int i = e / (R * R), r1 = (e / R) % R, r2 = e % R;
             double s = 0.0;
 #pragma unroll
@@ -490,7 +503,7 @@ __device__ __forceinline__ void spread_epilogue(const ColumnArgs& a, const Colum
         // Fpart is entry-major, [R^3+1][nblocks], so k_core_sum reads it coalesced
         const int nblocks = a.fstride > 0 ? a.fstride : a.S * g.K[0] * g.K[1];
         double* dst = a.Fpart + (int64_t)cr.seg * g.K[0] * g.K[1] + cr.col;
-        for (int e = threadIdx.x; e < R * R * R; e += 128) {
+        for (int e = threadIdx.x; e < R * R * R; e += NT_) {
             const int r0 = e / (R * R), rr = e % (R * R);
             double s = 0.0;
 #pragma unroll
@@ -498,16 +511,13 @@ __device__ __forceinline__ void spread_epilogue(const ColumnArgs& a, const Colum
             dst[(int64_t)e * nblocks] = s;
         }
         __syncthreads();
-        for (int o = 64; o > 0; o >>= 1) {
-            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) dst[(int64_t)R * R * R * nblocks] = red[0];
+        const double qs = block_tree_sum<NW>(red);
+        if (threadIdx.x == 0) dst[(int64_t)R * R * R * nblocks] = qs;
         return;
     }
     if (want_fwd) {
         double* dst = a.T1 + (int64_t)cr.seg * g.n[0] * g.n[1] * R;
-        for (int e = threadIdx.x; e < L2 * R; e += 128) {
+        for (int e = threadIdx.x; e < L2 * R; e += NT_) {
             const int ij = e / R, r = e % R, i = ij / L, j = ij % L;
             double s = 0.0;
 #pragma unroll
@@ -517,11 +527,8 @@ __device__ __forceinline__ void spread_epilogue(const ColumnArgs& a, const Colum
     }
     if (a.colq) {
         __syncthreads();
-        for (int o = 64; o > 0; o >>= 1) {
-            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) a.colq[(int64_t)cr.seg * g.K[0] * g.K[1] + cr.col] = red[0];
+        const double qs = block_tree_sum<NW>(red);
+        if (threadIdx.x == 0) a.colq[(int64_t)cr.seg * g.K[0] * g.K[1] + cr.col] = qs;
     }
 }
 
@@ -750,11 +757,14 @@ __device__ __forceinline__ int uv_swz(int row, int col) {
     return row * 8 + ((((col >> 1) ^ (row >> 1)) & 3) << 1) + (col & 1);
 }
 
-// CTA shared memory of k_spread_uv: 4 warp areas, the column's W2 (R x n2)
+#ifndef UV_NW
+#define UV_NW 4  // warps per column CTA of k_spread_uv
+#endif
+// CTA shared memory of k_spread_uv: UV_NW warp areas, the column's W2 (R x n2)
 // and the epilogue scratch.
 template <int L>
 __host__ __device__ constexpr size_t spread_uv_smem_doubles(int R, int n2) {
-    return 4 * (size_t)spread_uv_warp_doubles<L>(R) + (size_t)R * n2 +
+    return UV_NW * (size_t)spread_uv_warp_doubles<L>(R) + (size_t)R * n2 +
            (size_t)spread_epilogue_doubles(L, R);
 }
 
@@ -765,10 +775,10 @@ __host__ __device__ constexpr size_t spread_uv_smem_doubles(int R, int n2) {
 __device__ double* uv_scratch;
 // RTM: n-tiles of the W2 contraction held in registers (2: R <= 16, 4: R <= 32).
 template <int L, int RTM>
-__global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, int want_fwd) {
+__global__ void __launch_bounds__(32 * UV_NW, SPREAD_MINB) k_spread_uv(ColumnArgs a, int want_fwd) {
     using M = UvMap<L>;
     constexpr int L2 = M::L2, L3 = L2 * L, NT = M::NT, MT2 = M::MT2, KS2 = M::KS2, LDK = M::LDK;
-    constexpr int NW = 4;
+    constexpr int NW = UV_NW, NTH = 32 * NW;
     const Geometry& g = a.g;
     const int R = g.R, RT = (R + 7) / 8, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int RP = uv_t1_stride(R), n2 = g.n[2];
@@ -782,24 +792,24 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, in
     double* t1w = As + M::area;         // [MT2*8][RP]  warp partial of T1
     double* w2s = sm + NW * per_warp;   // [R][n2] W2 (monomial rows), shared by the CTA
     double* epi = w2s + R * n2;
-    __shared__ double red[128];
+    __shared__ double red[NTH];
     __shared__ int cst[66];             // cell starts of this column segment (+1)
     for (int e = lane; e < MT2 * 8 * RP; e += 32) t1w[e] = 0.0;
     for (int e = lane; e < M::ph; e += 32) ph[e] = 0.0;  // padding stays zero
-    for (int e0 = threadIdx.x; e0 < R * n2; e0 += 128 * 8) {  // loads in flight together
+    for (int e0 = threadIdx.x; e0 < R * n2; e0 += NTH * 8) {  // loads in flight together
         double v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-            if (e0 + 128 * u < R * n2) v[u] = __ldg(a.W2 + e0 + 128 * u);
+            if (e0 + NTH * u < R * n2) v[u] = __ldg(a.W2 + e0 + NTH * u);
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-            if (e0 + 128 * u < R * n2) w2s[e0 + 128 * u] = v[u];
+            if (e0 + NTH * u < R * n2) w2s[e0 + NTH * u] = v[u];
     }
     const int col_cell0 = (cr.c0 * g.K[1] + cr.c1) * g.K[2];
     const int nz = cr.ze - cr.zb;
     const bool cst_ok = nz + 1 <= 66;
     if (cst_ok)
-        for (int e = threadIdx.x; e <= nz; e += 128) cst[e] = a.start[col_cell0 + cr.zb + e];
+        for (int e = threadIdx.x; e <= nz; e += NTH) cst[e] = a.start[col_cell0 + cr.zb + e];
     const CellAxis ax0 = cell_axis_tab(a.cellax[0], cr.c0), ax1 = cell_axis_tab(a.cellax[1], cr.c1);
     // staging role: lane pair (p, h); fragment role: (gg, tg)
     const int p = lane & 15, h = lane >> 4;
@@ -970,7 +980,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_uv(ColumnArgs a, in
     const unsigned badw = __ballot_sync(0xffffffffu, !(tmax <= 1.0 + 2e-12));
     if (lane == 0 && badw) atomicOr(&a.bad[1], 1ull);
     if (UV_SKIP & 4) return;
-    spread_epilogue<L>(a, cr, sm, per_warp, M::area, RP, epi, red, qsum, want_fwd);
+    spread_epilogue<L, NW>(a, cr, sm, per_warp, M::area, RP, epi, red, qsum, want_fwd);
 }
 
 // Backward z-expansion + gather with compile-time L: psi for a batch of the
@@ -1415,9 +1425,9 @@ void launch_spread_uv_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
         }
     }
     if (a.g.R <= 16)
-        k_spread_uv<L, 2><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+        k_spread_uv<L, 2><<<grid, 32 * UV_NW, smem, s>>>(a, want_fwd ? 1 : 0);
     else
-        k_spread_uv<L, 4><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+        k_spread_uv<L, 4><<<grid, 32 * UV_NW, smem, s>>>(a, want_fwd ? 1 : 0);
     KB_CHECK_LAUNCH();
 }
 

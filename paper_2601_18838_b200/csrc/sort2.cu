@@ -38,6 +38,7 @@ constexpr int kTileWarps = 8;
 constexpr int kRounds = SORT2_ROUNDS;             // 32-particle rounds per warp
 constexpr int kTile = kTileWarps * kRounds * 32;  // particles per tile (2048)
 constexpr int kHistThreads = kTile / 4;           // 4 particles per thread
+constexpr int kMinTile = 4 * 32 * kTileWarps;     // the smallest k_tile_sort tile (TR = 4)
 constexpr int kGroup = 4;                         // rounds whose loads are issued together
 constexpr int kZWarps = 8;                        // warps per column CTA in k_z_sort
 constexpr int kZRounds = SORT2_ZROUNDS;
@@ -689,10 +690,10 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_sort(Geometry g,
 // and no scattered 32-byte record stores (scripts/probes/scatter_probe.cu).
 struct TileLayout {
     size_t rec, idx, wc, tc, cb, total;
-    __host__ __device__ explicit TileLayout(int ncol) {
+    __host__ __device__ TileLayout(int ncol, int tile) {
         rec = 0;
-        idx = rec + sizeof(double4) * kTile;
-        wc = idx + sizeof(int32_t) * kTile;
+        idx = rec + sizeof(double4) * tile;
+        wc = idx + sizeof(int32_t) * tile;
         tc = wc + ((sizeof(uint16_t) * kTileWarps * ncol + 15) & ~size_t(15));
         cb = tc + sizeof(int32_t) * ncol;
         total = cb + sizeof(int32_t) * (ncol + 1);
@@ -700,7 +701,9 @@ struct TileLayout {
 };
 constexpr size_t kTileMaxSmem = 200 * 1024;
 
-template <int CB>
+// TR rounds of 32 particles per warp: tiles of TR * 256 particles (the host
+// picks TR per launch to even out the last wave, launch_sort2_tiles).
+template <int CB, int TR>
 __global__ void __launch_bounds__(kTileWarps * 32, 2) k_tile_sort(Geometry g, int64_t n,
                                                                const double* __restrict__ xyz,
                                                                const double* __restrict__ q,
@@ -711,7 +714,8 @@ __global__ void __launch_bounds__(kTileWarps * 32, 2) k_tile_sort(Geometry g, in
     extern __shared__ __align__(16) unsigned char tsm[];
     __shared__ int32_t wsum[32];
     const int ncol = g.K[0] * g.K[1];
-    const TileLayout TL(ncol);
+    constexpr int kTT = TR * 32 * kTileWarps;
+    const TileLayout TL(ncol, kTT);
     double4* s_rec = reinterpret_cast<double4*>(tsm + TL.rec);
     int32_t* s_idx = reinterpret_cast<int32_t*>(tsm + TL.idx);
     uint16_t* wc = reinterpret_cast<uint16_t*>(tsm + TL.wc);  // [kTileWarps][ncol]
@@ -720,20 +724,21 @@ __global__ void __launch_bounds__(kTileWarps * 32, 2) k_tile_sort(Geometry g, in
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
     for (int e = tid; e < (int)((TL.tc - TL.wc) / 16); e += blockDim.x)
         reinterpret_cast<uint4*>(wc)[e] = make_uint4(0u, 0u, 0u, 0u);
-    const int64_t tbase = (int64_t)blockIdx.x * kTile;
-    const int64_t wbase = tbase + w * (kRounds * 32);
-    double4 rv[kRounds];
+    const int64_t tbase = (int64_t)blockIdx.x * kTT;
+    const int64_t wbase = tbase + w * (TR * 32);
+    double4 rv[TR];
 #pragma unroll
-    for (int r = 0; r < kRounds; ++r) {  // every load of the warp's slice in flight
+    for (int r = 0; r < TR; ++r) {  // every load of the warp's slice in flight
         const int64_t i = wbase + r * 32 + lane;
         if (i < n)
             rv[r] = make_double4(__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2),
                                  q ? __ldg(q + i) : 0.0);
     }
     const double b = __dmul_rn(2.0, g.radius), y = g.inv_diam;
-    int colr[kRounds];
+    const bool zblock = g.z_lo > 0 || g.z_hi < g.K[2];
+    int colr[TR];
 #pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
+    for (int r = 0; r < TR; ++r) {
         const int64_t i = wbase + r * 32 + lane;
         colr[r] = -1;
         if (i < n) {
@@ -743,7 +748,8 @@ __global__ void __launch_bounds__(kTileWarps * 32, 2) k_tile_sort(Geometry g, in
                 atomicMin(&bad[0], (unsigned long long)i);  // Box3::contains (geometry.hpp:36-40)
             const int c0 = axis_cell2(p0, g.center[0], g.radius, g.K[0], b, y);
             const int c1 = axis_cell2(p1, g.center[1], g.radius, g.K[1], b, y);
-            const int c2 = axis_cell2(p2, g.center[2], g.radius, g.K[2], b, y);
+            // c2 only for plans with a z block (a clamped c2 is always in [0, K2))
+            const int c2 = zblock ? axis_cell2(p2, g.center[2], g.radius, g.K[2], b, y) : g.z_lo;
             if (c0 < g.x_lo || c0 >= g.x_hi || c1 < g.y_lo || c1 >= g.y_hi || c2 < g.z_lo || c2 >= g.z_hi)
                 atomicOr(&bad[1], 2ull);  // not in this plan's cell block
             colr[r] = c0 * g.K[1] + c1;
@@ -751,9 +757,9 @@ __global__ void __launch_bounds__(kTileWarps * 32, 2) k_tile_sort(Geometry g, in
     }
     __syncthreads();
     // 1: per-warp column counts (peer masks kept for the placement)
-    unsigned pk[kRounds];
+    unsigned pk[TR];
 #pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
+    for (int r = 0; r < TR; ++r) {
         const bool act = colr[r] >= 0;
         const int col = act ? colr[r] : -1 - lane;
         const unsigned peers = warp_peers<CB>(col);
@@ -780,7 +786,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, 2) k_tile_sort(Geometry g, in
     for (int c = tid; c <= ncol; c += blockDim.x) trow[c] = cb[c];
     // 3: placement in index order into the staged tile
 #pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
+    for (int r = 0; r < TR; ++r) {
         const bool act = colr[r] >= 0;
         const unsigned peers = pk[r];
         int base = 0;
@@ -842,7 +848,7 @@ struct ZTilesLayout {
 };
 
 template <int ZB>
-__global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n, int ntiles,
+__global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n, int ntiles, int tile,
                                                         int whole_cap,
                                                         const int32_t* __restrict__ toff,
                                                         const int32_t* __restrict__ idx2,
@@ -905,7 +911,7 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n,
         int32_t* srca = pre + ntiles + 1;
         for (int t = lo; t < hi; ++t) {
             const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
-            srca[t] = t * kTile + a;
+            srca[t] = t * tile + a;
             pre[t] = run;
             run += __ldg(toff + (int64_t)t * (ncol + 1) + col + 1) - a;
         }
@@ -928,14 +934,14 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n,
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if (lo + u < hi) {
-                const int c = e_[u] - a_[u], src0 = (lo + u) * kTile + a_[u];
+                const int c = e_[u] - a_[u], src0 = (lo + u) * tile + a_[u];
                 for (int k = 0; k < c; ++k) s_idx[run + k] = src0 + k;
                 run += c;
             }
     } else {
         for (int t = lo; t < hi; ++t) {
             const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
-            const int c = __ldg(toff + (int64_t)t * (ncol + 1) + col + 1) - a, src0 = t * kTile + a;
+            const int c = __ldg(toff + (int64_t)t * (ncol + 1) + col + 1) - a, src0 = t * tile + a;
             for (int k = 0; k < c; ++k) s_idx[run + k] = src0 + k;
             run += c;
         }
@@ -978,7 +984,7 @@ bool sort2_supported(const Geometry& g) {
 }
 
 size_t sort2_hist_entries(const Geometry& g, int64_t cap) {  // also the tile path's toff
-    const int64_t ntiles = (cap + kTile - 1) / kTile;
+    const int64_t ntiles = (cap + kMinTile - 1) / kMinTile;
     return ((size_t)g.K[0] * g.K[1] + 1) * (size_t)std::max<int64_t>(1, ntiles);
 }
 
@@ -996,27 +1002,68 @@ static bool tiles_chosen(int ncol) {
     return m == 1 || (m == 2 && ncol * 4 <= kTile);
 }
 
+template <class F>
+auto pick_rounds(int tr, F f) {
+    switch (tr) {
+        case 4: return f(std::integral_constant<int, 4>{});
+        case 7: return f(std::integral_constant<int, 7>{});
+        default: return f(std::integral_constant<int, 8>{});
+    }
+}
+
 static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, const SortBuffers& b,
                                cudaStream_t s, int* launches, const double* q, double4* sp) {
     const int ncol = g.K[0] * g.K[1];
-    const int ntiles = (int)std::max<int64_t>(1, (n + kTile - 1) / kTile);
-    const TileLayout TL(ncol);
+    if (!tiles_chosen(ncol)) return false;
+    // Tile rounds: the fewest (waves x tile length) at two CTAs per SM, among
+    // tiles holding >= 4 particles per column on average (the pieces k_z_tiles
+    // gathers); ties go to the longer tile. Config 3: 559 tiles of 1792.
+    static int slots = 0;
+    if (!slots) {
+        int dev = 0, sms = 0;
+        KB_CUDA(cudaGetDevice(&dev));
+        KB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        slots = 2 * sms;
+    }
+    int tr = 8;
+    {
+        int64_t best = -1;
+        for (int cand : {8, 7, 4}) {
+            const int tile = cand * 32 * kTileWarps;
+            if (tile < 4 * ncol) continue;
+            const int64_t nt = std::max<int64_t>(1, (n + tile - 1) / tile);
+            const int64_t cost = (nt + slots - 1) / slots * cand;
+            if (best < 0 || cost < best) {
+                best = cost;
+                tr = cand;
+            }
+        }
+    }
+    const int tile = tr * 32 * kTileWarps;
+    const int ntiles = (int)std::max<int64_t>(1, (n + tile - 1) / tile);
+    const TileLayout TL(ncol, tile);
     const int wcap = whole_cap_for(g.K[2]);
     const ZTilesLayout ZL(g.K[2], ntiles, wcap);
-    if (!tiles_chosen(ncol) || TL.total > kTileMaxSmem || ntiles > 65535 || ZL.total_chunked > 160 * 1024)
-        return false;
+    if (TL.total > kTileMaxSmem || ntiles > 65535 || ZL.total_chunked > 160 * 1024) return false;
     const int cb = (bits_for(ncol) + 1) & ~1, zb = (bits_for(g.K[2]) + 1) & ~1;
     static bool attr = false;
     if (!attr) {
         for (int bb = 2; bb <= 16; bb += 2) {
-            KB_CUDA(cudaFuncSetAttribute(pick_bits(bb, [](auto B) { return &k_tile_sort<decltype(B)::value>; }),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileMaxSmem));
+            for (int r : {4, 7, 8})
+                KB_CUDA(cudaFuncSetAttribute(pick_bits(bb, [r](auto B) {
+                                                 return pick_rounds(r, [](auto T) {
+                                                     return &k_tile_sort<decltype(B)::value, decltype(T)::value>;
+                                                 });
+                                             }),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileMaxSmem));
             KB_CUDA(cudaFuncSetAttribute(pick_bits(bb, [](auto B) { return &k_z_tiles<decltype(B)::value>; }),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
         }
         attr = true;
     }
-    auto tile_kernel = pick_bits(cb, [](auto B) { return &k_tile_sort<decltype(B)::value>; });
+    auto tile_kernel = pick_bits(cb, [tr](auto B) {
+        return pick_rounds(tr, [](auto T) { return &k_tile_sort<decltype(B)::value, decltype(T)::value>; });
+    });
     auto z_kernel = pick_bits(zb, [](auto B) { return &k_z_tiles<decltype(B)::value>; });
     int l = 0;
     if (n > 0) {
@@ -1026,10 +1073,9 @@ static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, 
     } else {
         KB_CUDA(cudaMemsetAsync(b.hist, 0, sizeof(int32_t) * (ncol + 1), s));
     }
-    // the piece tables alias the z counters only when they fit there
     const int whole_cap = wcap > 0 && ZL.total_whole <= kZWholeMaxSmem ? wcap : 0;
     const size_t zsmem = std::max(ZL.total_chunked, whole_cap ? ZL.total_whole : 0);
-    z_kernel<<<ncol, kZThreads, zsmem, s>>>(g, n, ntiles, whole_cap, b.hist, b.idx2, b.rec, b.perm,
+    z_kernel<<<ncol, kZThreads, zsmem, s>>>(g, n, ntiles, tile, whole_cap, b.hist, b.idx2, b.rec, b.perm,
                                             b.start, sp);
     KB_CHECK_LAUNCH();
     ++l;

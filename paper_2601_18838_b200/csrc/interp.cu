@@ -1373,9 +1373,20 @@ size_t spread_smem(const Geometry& g) {
                              (size_t)kChunk * 3 * L);
 }
 
-int gather_batch(const Geometry& g) {
+#ifndef GATHER_BATCH_KB
+#define GATHER_BATCH_KB 24  // shared memory for the batch's cell coefficients
+#endif
+// Cells per gather batch: 24 KB of coefficients, or the whole column segment
+// when it fits in 40 KB and the column CTAs make one wave at three per SM
+// (each batch costs a serial load -> expand -> evaluate round; config 3: one
+// batch of 21 cells, 47.8 -> 46.4 us). Grids of many columns keep the smaller
+// batch: their fourth CTA per SM is worth more (config 4: 192 vs 204 us).
+int gather_batch(const Geometry& g, int S = 1) {
     const int L3 = g.L * g.L * g.L;
-    const int cap = (24 * 1024) / (int)(sizeof(double) * L3);
+    const int seg = (g.z_hi - g.z_lo + S - 1) / std::max(1, S);
+    if (block_columns(g) * S <= 3 * 148 && seg <= kGatherTab && (size_t)seg * L3 * sizeof(double) <= 40 * 1024)
+        return std::max(1, seg);
+    const int cap = (GATHER_BATCH_KB * 1024) / (int)(sizeof(double) * L3);
     return cap < 1 ? 1 : cap;
 }
 
@@ -1460,9 +1471,9 @@ void launch_gather_t(const ColumnArgs& a0, int mode, cudaStream_t s) {
 #endif
     const int grid = block_columns(a.g) * a.S;
 #ifdef GATHER_CB
-    const int cb = std::min(gather_batch(a.g), GATHER_CB);
+    const int cb = std::min(gather_batch(a.g, a.S), GATHER_CB);
 #else
-    const int cb = gather_batch(a.g);
+    const int cb = gather_batch(a.g, a.S);
 #endif
     const int R = a.g.R;
     const size_t smem = sizeof(double) * ((size_t)L * L * R + (size_t)cb * L * L * L +

@@ -222,6 +222,26 @@ def timed_steps(torch, fn, steps, flush):
     return times
 
 
+def mesh_work(w, ms):
+    """Mesh GFLOP/s (BASELINE's second metric) for the SKP operator as executed:
+    the term-collapsed form, (W0 (x) W1 (x) W2) then G .* then the transposes,
+    2 (2 R n^3 + 2 R^2 n^2 + 2 R^3 n) + R^3 flops with R = 2M+1,
+    fused into the spread and gather kernels, so it is quoted per whole step.
+    Beside it, the reference's per-term SPKMV flops 12 |Lambda| r_ax n^3
+    (r_ax = 2(M+1), SURVEY.md §8(d) F form) over the same step time: the
+    throughput the reference's formulation would need to match this step."""
+    L, M = w.order, w.cfg.modes
+    R, r_ax = 2 * M + 1, 2 * (M + 1)
+    n = [k * L for k in w.grid.counts]
+    n3 = float(n[0] * n[1] * n[2])
+    collapsed = 2.0 * (2 * R * n3 + 2 * R * R * n[0] * n[1] + 2 * R ** 3 * n[0]) + R ** 3
+    spkmv = 12.0 * len(w.dec.terms) * r_ax * n3
+    return {"formulation": "collapsed (fused into spread/gather; per whole step)",
+            "collapsed_flops": collapsed, "gflops": collapsed / (ms * 1e-3) / 1e9,
+            "reference_spkmv_flops": spkmv,
+            "reference_spkmv_equivalent_gflops": spkmv / (ms * 1e-3) / 1e9}
+
+
 def spread_algorithmic(w, S):
     """Algorithmic work of the fused spread + forward-z kernel per launch
     (DESIGN.md §4): flops 2 L^3 N (accumulate) + 2 R L^3 per cell
@@ -384,6 +404,7 @@ def run_ours(a):
         return
 
     value = w.n / (ms * 1e-3)
+    mesh = mesh_work(w, ms)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -400,6 +421,7 @@ def run_ours(a):
                          "NCCL core all-reduce, backward, D2H" if slab else
                          "KpmePlan.execute_host_ptr -> kpme_gpu_plan_execute (pinned host "
                          "xyz/q in, potentials out)")},
+        "mesh": mesh,
         "gpu_launches": launches * a.steps,
         "clocks": clk,
         "roofline": roofline,

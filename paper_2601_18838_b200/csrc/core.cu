@@ -171,19 +171,14 @@ __global__ void k_core_sum(int nblocks, int E, const double* __restrict__ Fpart,
     const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (e >= E) return;
     const double* row = Fpart + (int64_t)e * nblocks;
-    // four independent partial sums: four loads in flight per lane per step
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    double s0 = 0.0, s1 = 0.0;
     int b = lane;
-    for (; b + 96 < nblocks; b += 128) {
-        const double v0 = __ldg(row + b), v1 = __ldg(row + b + 32), v2 = __ldg(row + b + 64),
-                     v3 = __ldg(row + b + 96);
-        s0 += v0;
-        s1 += v1;
-        s2 += v2;
-        s3 += v3;
+    for (; b + 32 < nblocks; b += 64) {
+        s0 += row[b];
+        s1 += row[b + 32];
     }
-    for (; b < nblocks; b += 32) s0 += __ldg(row + b);
-    double s = (s0 + s1) + (s2 + s3);
+    if (b < nblocks) s0 += row[b];
+    double s = s0 + s1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) F[e] = s;

@@ -987,7 +987,10 @@ __global__ void __launch_bounds__(32 * UV_NW, SPREAD_MINB) k_spread_uv(ColumnArg
 // column's cells in shared memory, then one thread per particle,
 // z = sum_i w0[i] sum_j w1[j] sum_k w2[k] psi[i][j][k] - c_Lambda sum(q),
 // scattered straight to global particle order.
-constexpr int GT = 128;  // gather threads per CTA
+#ifndef GATHER_GT
+#define GATHER_GT 128
+#endif
+constexpr int GT = GATHER_GT;  // gather threads per CTA
 
 constexpr int kGatherTab = 32;  // batch cells with shared-memory start/axis tables
 template <int L, int MODE, bool MONO>

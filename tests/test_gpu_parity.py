@@ -519,3 +519,18 @@ def test_sort_variants_forced(variant):
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.parametrize("n", [600_000, 250_000])
+def test_sort_tile_lengths(oracle, n):
+    """The tile sort's per-launch tile length (sort2.cu launch_sort2_tiles):
+    600k particles on 441 columns take 2048-particle tiles (one full wave),
+    250k take 1792; config 1-3 shapes cover 1024 and 1792. Bit-exact."""
+    from oracle.binding import make_problem
+
+    pb = make_problem(oracle, n=n, counts=21, order=4, eps=1e-6, seed=5)
+    plan = plan_for(pb)
+    perm, start = plan.sort(dev(pb.pos))
+    operm, ostart = oracle.assign_particles(*UNIT, (21, 21, 21), pb.pos)
+    np.testing.assert_array_equal(start.cpu().numpy(), ostart)
+    np.testing.assert_array_equal(perm.cpu().numpy(), operm)

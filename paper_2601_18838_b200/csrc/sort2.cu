@@ -860,9 +860,9 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n,
     __shared__ int32_t wsum[32];
     const int col = blockIdx.x, ncol = g.K[0] * g.K[1], K2 = g.K[2];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    // the piece of every tile (thread-contiguous slices of tiles, so the scan
-    // is in tile order) into the tables past the chunked layout; the whole
-    // path's (aliasing its z counters) gets them copied once m is known
+    // every tile's piece of this column: thread-contiguous slices of tiles, so
+    // the scan below is in tile order; the column base cs sums the pieces'
+    // offsets and m their lengths
     const int per = (ntiles + kZThreads - 1) / kZThreads;
     const int lo = min(ntiles, tid * per), hi = min(ntiles, lo + per);
     const ZTilesLayout TL(K2, ntiles, whole_cap);

@@ -225,9 +225,15 @@ __global__ void __launch_bounds__(kTileWarps * 32, 4) k_col_scatter(Geometry g, 
                                                                  const double* __restrict__ q,
                                                                  int32_t* __restrict__ idx2,
                                                                  double4* __restrict__ rec2) {
-    extern __shared__ int32_t wc[];  // [kTileWarps][ncol] per-warp column counters, then bases
+    // [kTileWarps][ncol] per-warp column counters, then offsets inside the
+    // tile's column segment (16-bit: a tile holds kTile particles), and the
+    // tile's global column bases [ncol] (half the shared memory of 32-bit
+    // counters: a fourth CTA per SM on large grids)
+    extern __shared__ int32_t csm[];
+    uint16_t* wc = reinterpret_cast<uint16_t*>(csm);
     __shared__ unsigned pm[kTileWarps][kRounds][32];  // phase-1 peer masks, reused in phase 3
     const int ncol = g.K[0] * g.K[1];
+    int32_t* cbs = csm + (kTileWarps * ncol + 1) / 2;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int e = threadIdx.x; e < kTileWarps * ncol; e += blockDim.x) wc[e] = 0;
     const int64_t wbase = (int64_t)blockIdx.x * kTile + w * (kRounds * 32);
@@ -245,16 +251,17 @@ __global__ void __launch_bounds__(kTileWarps * 32, 4) k_col_scatter(Geometry g, 
         const int col = act ? kreg[r] >> 16 : -1 - lane;
         const unsigned peers = warp_peers<CB>(col);
         pm[w][r][lane] = peers;
-        if (act && lane == __ffs(peers) - 1) wc[w * ncol + col] += __popc(peers);
+        if (act && lane == __ffs(peers) - 1) wc[w * ncol + col] += (uint16_t)__popc(peers);
         __syncwarp();
     }
     __syncthreads();
-    // 2: exclusive prefix over warps, plus this tile's global column offset
+    // 2: exclusive prefix over warps; this tile's global column offset
     for (int c = threadIdx.x; c < ncol; c += blockDim.x) {
-        int run = cbase[c] + cscan[(int64_t)c * ntiles + blockIdx.x];
+        cbs[c] = cbase[c] + cscan[(int64_t)c * ntiles + blockIdx.x];
+        int run = 0;
         for (int k = 0; k < kTileWarps; ++k) {
             const int t = wc[k * ncol + c];
-            wc[k * ncol + c] = run;
+            wc[k * ncol + c] = (uint16_t)run;
             run += t;
         }
     }
@@ -275,11 +282,14 @@ __global__ void __launch_bounds__(kTileWarps * 32, 4) k_col_scatter(Geometry g, 
             const bool act = k >= 0;
             const int col = act ? k >> 16 : -1 - lane;
             const unsigned peers = pm[w][r0 + u][lane];
-            int base = 0;
-            if (act) base = wc[w * ncol + col];
-            pos[u] = base + __popc(peers & ((1u << lane) - 1));
+            int rel = 0, base = 0;
+            if (act) {
+                rel = wc[w * ncol + col];
+                base = cbs[col];
+            }
+            pos[u] = base + rel + __popc(peers & ((1u << lane) - 1));
             __syncwarp();
-            if (act && lane == __ffs(peers) - 1) wc[w * ncol + col] = base + __popc(peers);
+            if (act && lane == __ffs(peers) - 1) wc[w * ncol + col] = (uint16_t)(rel + __popc(peers));
             __syncwarp();
         }
 #pragma unroll
@@ -1119,7 +1129,7 @@ void launch_sort2(const Geometry& g, int64_t n, const double* xyz, const SortBuf
     KB_CHECK_LAUNCH();
     ++l;
     if (n > 0) {
-        col_kernel<<<ntiles, kTileWarps * 32, (kTileWarps * ncol + ncol + 1) * sizeof(int32_t),
+        col_kernel<<<ntiles, kTileWarps * 32, ((kTileWarps * ncol + 1) / 2 + ncol) * sizeof(int32_t),
                         s>>>(g, n, ntiles, b.key, b.hist, b.cbase, xyz, q, b.idx2, b.rec);
         KB_CHECK_LAUNCH();
         ++l;

@@ -1377,20 +1377,25 @@ size_t spread_smem(const Geometry& g) {
 }
 
 #ifndef GATHER_BATCH_KB
-#define GATHER_BATCH_KB 24  // shared memory for the batch's cell coefficients
+#define GATHER_BATCH_KB 28  // shared memory for the batch's cell coefficients
 #endif
-// Cells per gather batch: 24 KB of coefficients, or the whole column segment
-// when it fits in 40 KB and the column CTAs make one wave at three per SM
-// (each batch costs a serial load -> expand -> evaluate round; config 3: one
-// batch of 21 cells, 47.8 -> 46.4 us). Grids of many columns keep the smaller
-// batch: their fourth CTA per SM is worth more (config 4: 192 vs 204 us).
+// Cells per gather batch: 28 KB of coefficients in equal batches, or the
+// whole column segment when it fits in 40 KB and the column CTAs make one
+// wave at three per SM (each batch costs a serial load -> expand -> evaluate
+// round; config 3: one batch of 21 cells, 47.8 -> 46.4 us). Grids of many
+// columns keep the smaller batch: their fourth CTA per SM is worth more
+// (config 4: 3 rounds of 15/14/14 cells, 185 us; 40 KB batches 204 us;
+// 24 KB, 4 rounds, 192 us).
 int gather_batch(const Geometry& g, int S = 1) {
     const int L3 = g.L * g.L * g.L;
     const int seg = (g.z_hi - g.z_lo + S - 1) / std::max(1, S);
     if (block_columns(g) * S <= 3 * 148 && seg <= kGatherTab && (size_t)seg * L3 * sizeof(double) <= 40 * 1024)
         return std::max(1, seg);
-    const int cap = (GATHER_BATCH_KB * 1024) / (int)(sizeof(double) * L3);
-    return cap < 1 ? 1 : cap;
+    const int cap = std::max(1, (GATHER_BATCH_KB * 1024) / (int)(sizeof(double) * L3));
+    // equal batches for the same number of rounds: no short tail round
+    // (config 4: 43 cells as 11 + 11 + 11 + 10, not 14 + 14 + 14 + 1)
+    const int rounds = (std::max(1, seg) + cap - 1) / cap;
+    return (std::max(1, seg) + rounds - 1) / rounds;
 }
 
 

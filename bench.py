@@ -132,59 +132,63 @@ class Clocks:
 
 
 # ---- CPU reference / baseline ----------------------------------------------------
-
-def cpu_problem(w, nterms=None):
-    from oracle.binding import Problem
-
-    tw, prof = w.dec.arrays()
-    if nterms is not None:
-        tw, prof = tw[:nterms], prof[:nterms]
-    return Problem(xi=w.cfg.xi, modes=w.cfg.modes, center=w.grid.box.center,
-                   radius=w.grid.box.radius, counts=w.grid.counts, order=w.order,
-                   term_weights=tw, profiles=prof, correction=w.dec.correction,
-                   pos=w.data.cloud.positions, q=w.data.charges.values)
-
+# Everything here goes through oracle/ only (test infrastructure, the CPU arm):
+# inputs from the back end's own sample_cloud / sinc_rule_for_eps /
+# skp_from_quadrature (oracle/workloads.py), never from the GPU library.
 
 def cpu_runner():
-    """oracle/_ref (the reference's own headers, built here) when present,
-    else the oracle port."""
+    """oracle/_ref at the reference's Release flags (-O3 -DNDEBUG) when
+    present, else the -O2 parity build, else the oracle port."""
     from oracle.binding import CpuKpme
 
-    try:
-        return CpuKpme("ref"), "reference"
-    except FileNotFoundError:
-        return CpuKpme("oracle"), "port"
+    for which, kind, build in (("ref_o3", "reference", "oracle/_ref/libkpme_ref_o3.so "
+                                "(reference headers, -O3 -DNDEBUG = CMake Release)"),
+                               ("ref", "reference", "oracle/_ref/libkpme_ref.so "
+                                "(reference headers, -O2 -ffp-contract=off)"),
+                               ("oracle", "port", "oracle/build/libkpme_oracle.so (C port, -O2)")):
+        try:
+            return CpuKpme(which), kind, build
+        except FileNotFoundError:
+            continue
+    raise FileNotFoundError("no CPU back end built (run __graft_entry__.build())")
 
 
-def cpu_time(cpu, w, nterms, threads):
-    pb = cpu_problem(w, nterms)
+def cpu_time(cpu, pb, nterms, threads):
+    from dataclasses import replace
+
+    sub = replace(pb, term_weights=pb.term_weights[:nterms], profiles=pb.profiles[:nterms])
     t0 = time.perf_counter()
-    cpu.kpme_apply(pb, threads=threads)
+    cpu.kpme_apply(sub, threads=threads)
     return time.perf_counter() - t0
 
 
-def cpu_sampled(w, budget_s, threads, reps=1):
+def cpu_sampled(name, budget_s, threads, reps=1):
     """Bounded sample of the full workload: the reference's kpme_apply on the
     full particle set and cell grid with the first s SKP terms, plus one run
     with no terms. Its cost is exactly affine in the term count (one spkmv and
     one factor build per term, parallel.hpp:193-196, 265-279), so the full-
     |Lambda| time is t0 + |Lambda| (t_s - t0) / s."""
-    cpu, kind = cpu_runner()
-    nt = len(w.dec.terms)
-    t0 = cpu_time(cpu, w, 0, threads)
-    t1 = cpu_time(cpu, w, 1, threads)
+    from oracle import workloads
+
+    cpu, kind, build = cpu_runner()
+    pb = workloads.problem(name, cpu)
+    n = len(pb.q)
+    nt = len(pb.term_weights)
+    t0 = cpu_time(cpu, pb, 0, threads)
+    t1 = cpu_time(cpu, pb, 1, threads)
     per = max(t1 - t0, 1e-6)
     s = int(max(1, min(nt, (budget_s - t0) / per)))
     samples = []
     for _ in range(reps):
-        ts = cpu_time(cpu, w, s, threads)
+        ts = cpu_time(cpu, pb, s, threads)
         samples.append(t0 + nt * (ts - t0) / s)
     full = statistics.median(samples)
-    sample = (f"{w.name}: full {w.n} particles and {w.grid.counts} cells, first {s} of {nt} "
+    sample = (f"{name}: full {n} particles and {list(pb.counts)} cells, first {s} of {nt} "
               f"SKP terms (+ one 0-term run, t0={t0:.2f}s); full-|Lambda| time extrapolated "
-              f"affinely in the term count" if s < nt else f"{w.name}: full workload")
-    return {"value": w.n / full, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
-            "seconds_full_equiv": full}, samples
+              f"affinely in the term count" if s < nt else f"{name}: full workload")
+    return {"value": n / full, "unit": UNIT, "cores": threads, "kind": kind, "build": build,
+            "sample": sample, "seconds_full_equiv": full,
+            "inputs": "built by the same back end (oracle/workloads.py)"}, samples, pb
 
 
 # ---- GPU helpers ------------------------------------------------------------------
@@ -410,10 +414,11 @@ def run_ours(a):
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded splitmix64 sample_cloud, BASELINE.json config shapes)",
-        "config": {**w.describe(), "formulation": "collapsed (term-collapsed SKP core, "
-                   "per-shape chooser)", "parallelism": (f"rank grid {'x'.join(map(str, plan.dims))} of cell blocks "
-                                   f"(NCCL core all-reduce)") if slab else "1 GPU",
-                   "l2": "flushed (256 MiB write) before every timed step"},
+        "config": w.describe(),
+        "impl_config": {"formulation": "collapsed (term-collapsed SKP core, per-shape chooser)",
+                        "parallelism": (f"rank grid {'x'.join(map(str, plan.dims))} of cell "
+                                        f"blocks (NCCL core all-reduce)") if slab else "1 GPU",
+                        "l2": "flushed (256 MiB write) before every timed step"},
         "e2e": {"value": w.n / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "ms_per_step_spread": e2e_spread,
                 "h2d_bytes_per_step": 32 * w.n, "d2h_bytes_per_step": 8 * w.n,
@@ -429,7 +434,7 @@ def run_ours(a):
         **meta,
     }
     if world == 1 and not slab and not a.no_cpu_baseline:
-        cb, _ = cpu_sampled(w, 20.0, os.cpu_count() or 1)
+        cb, _, _ = cpu_sampled(a.workload, 20.0, os.cpu_count() or 1)
         cb["cpu"] = cpu_info()
         line["cpu_baseline"] = cb
     if world == 1 and not slab and not a.no_extras:
@@ -477,26 +482,28 @@ def extras(torch, dev, flush, steps):
 
 
 def run_reference(a):
-    """The reference's own CPU implementation (oracle/_ref; else the oracle
-    port) with every host thread, on bounded samples of the same workload."""
+    """The reference's own CPU implementation (oracle/_ref at Release flags;
+    else the oracle port) with every host thread, on bounded samples of the
+    same workload. Never imports the GPU package: inputs come from the same
+    back end (oracle/workloads.py)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from paper_2601_18838_b200 import inputs
+    from oracle import workloads
 
-    w = inputs.workload(a.workload)
     threads = os.cpu_count() or 1
     budget = max(3.0, min(20.0, 200.0 / max(1, a.steps + a.warmup)))
-    cb, samples = cpu_sampled(w, budget, threads, reps=a.steps + a.warmup)
+    cb, samples, pb = cpu_sampled(a.workload, budget, threads, reps=a.steps + a.warmup)
     timed = samples[a.warmup:] or samples
     full = statistics.median(timed)
-    value = w.n / full
+    value = len(pb.q) / full
     cb["value"] = value
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": full * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded splitmix64 sample_cloud, BASELINE.json config shapes)",
-            "config": {**w.describe(), "parallelism": f"CPU, {threads} threads"},
+            "config": workloads.describe(a.workload, len(pb.term_weights)),
+            "impl_config": {"parallelism": f"CPU, {threads} threads", "build": cb["build"]},
             "impl": "reference", "cpu_baseline": {**cb, "cpu": cpu_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}

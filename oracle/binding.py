@@ -8,6 +8,8 @@ Two back ends with the same interface:
   headers compiled here against the clean-room Eigen subset
   (oracle/ref/Makefile). Only exists where /root/reference was present at
   build time (it travels to the GPU box as a built file).
+* ``CpuKpme("ref_o3")`` -> oracle/_ref/libkpme_ref_o3.so, the same shim at
+  the reference's Release flags; the build bench.py times.
 """
 from __future__ import annotations
 
@@ -21,6 +23,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIBS = {
     "oracle": (os.path.join(HERE, "build", "libkpme_oracle.so"), "ko_"),
     "ref": (os.path.join(HERE, "_ref", "libkpme_ref.so"), "kr_"),
+    # the same shim at the reference's CMake Release flags (-O3 -DNDEBUG):
+    # what bench.py times; "ref" (-O2 -ffp-contract=off) is the parity pin
+    "ref_o3": (os.path.join(HERE, "_ref", "libkpme_ref_o3.so"), "kr_"),
 }
 
 _dp = C.POINTER(C.c_double)

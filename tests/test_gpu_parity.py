@@ -303,8 +303,8 @@ def test_host_path_chunks(oracle, chunks):
 
 @pytest.mark.parametrize("molecules,K", [(30000, 13), (300000, 29)])
 def test_e2e_water_vs_oracle(oracle, molecules, K):
-    """Config 4's water recipe at 9e4 and 9e5 sites (config 4 itself needs
-    ~25 GB in the reference layout): device path and pipelined host path
+    """Config 4's water recipe at 9e4 and 9e5 sites (config 4 itself at 3e6
+    sites is tests/test_gpu_configs.py): device path and pipelined host path
     against the oracle at 1e-10. Neutral molecules make the zero mode a
     difference of two rounded sums in the reference; the GPU evaluates it
     exactly, so the residual is the oracle's own rounding."""

@@ -283,3 +283,44 @@ def test_reference_acceptance_gate_runs():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("PASS criterion") == 8
+
+
+# ---- oracle/workloads.py (inputs of the CPU bench arm) ----------------------
+
+_HAS_REF = os.path.exists(os.path.join(os.path.dirname(__file__), "..", "oracle", "_ref",
+                                       "libkpme_ref.so"))
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_workloads_match_package_inputs(oracle, name):
+    """bench.py's reference arm builds its inputs through the CPU back end
+    alone (never the GPU library). They must be bit-identical to the
+    package's (paper_2601_18838_b200.inputs), for the oracle port and for the
+    reference's own headers."""
+    from oracle import workloads
+    from paper_2601_18838_b200 import inputs
+
+    w = inputs.workload(name)
+    tw, prof = w.dec.arrays()
+    backs = [oracle] + ([CpuKpme("ref"), CpuKpme("ref_o3")] if _HAS_REF else [])
+    for cpu in backs:
+        pb = workloads.problem(name, cpu)
+        assert np.array_equal(pb.pos, w.data.cloud.positions)
+        assert np.array_equal(pb.q, w.data.charges.values)
+        assert np.array_equal(pb.term_weights, tw) and np.array_equal(pb.profiles, prof)
+        assert pb.correction == w.dec.correction and pb.counts == tuple(w.grid.counts)
+        assert workloads.describe(name, len(tw)) == w.describe()
+
+
+@pytest.mark.skipif(not _HAS_REF, reason="oracle/_ref not built (no /root/reference)")
+def test_dense_factors_oracle_vs_reference(oracle):
+    """Config 5's factors assembled from build_uv: oracle port == reference
+    headers, bit for bit; each A_a(lambda) is symmetric-shaped n x n with the
+    cell-block structure U_c V_c'."""
+    from oracle import workloads
+
+    a = workloads.dense_factors(oracle, 32, 6)
+    b = workloads.dense_factors(CpuKpme("ref"), 32, 6)
+    for x, y in zip(a, b):
+        assert x.shape == (6, 32, 32)
+        assert np.array_equal(x, y)

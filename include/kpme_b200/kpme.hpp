@@ -11,7 +11,9 @@
 // (via NumericalError) kpme::numerical_error.
 #pragma once
 
+#include <array>
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
@@ -42,6 +44,35 @@ struct GpuOptions {
     int device = 0;
     int formulation = KPME_GPU_FORM_AUTO;
     bool ledger = true;  // synthesise KpmeResult::ledger
+    // More than one device: one process drives them all (a multi-device plan:
+    // cell blocks per device, partial cores summed over NVLink peer memory or
+    // NCCL). Empty: `device` alone.
+    std::vector<int> devices;
+
+    // Defaults for calls that carry no GPU options (the reference signature):
+    // KPME_GPU_DEVICES="0,1,2,3" (a device list) or KPME_GPU_DEVICE=<n>.
+    static GpuOptions from_env() {
+        GpuOptions g;
+        if (const char* e = std::getenv("KPME_GPU_DEVICE")) g.device = std::atoi(e);
+        if (const char* e = std::getenv("KPME_GPU_DEVICES")) {
+            const std::string s(e);
+            std::size_t i = 0;
+            while (i < s.size()) {
+                std::size_t j = s.find(',', i);
+                if (j == std::string::npos) j = s.size();
+                if (j > i) g.devices.push_back(std::atoi(s.substr(i, j - i).c_str()));
+                i = j + 1;
+            }
+            if (!g.devices.empty()) g.device = g.devices[0];
+        }
+        return g;
+    }
+};
+
+// KpmeOptions defaults (parallel.hpp:230-233) for calls that omit them.
+struct DefaultOptions {
+    bool fuse_terms = false;
+    int threads = 1;
 };
 
 template <class NumericalError = numerical_error>
@@ -99,9 +130,29 @@ kpme_gpu_config make_config(const Cfg& cfg, const Grid& grid, int order, const D
     c.profiles = f.profiles.data();
     c.fuse_terms = opt.fuse_terms ? 1 : 0;
     c.threads = opt.threads;
-    c.device = gpu.device;
+    c.device = gpu.devices.empty() ? gpu.device : gpu.devices[0];
     c.formulation = gpu.formulation;
+    c.ndevices = int(gpu.devices.size());
+    c.devices = gpu.devices.empty() ? nullptr : gpu.devices.data();
     return c;
+}
+
+// PointCloud::positions as double[n][3]: the reference's
+// std::vector<std::array<double, 3>> already has that layout, so it is passed
+// through without a copy; other position types are copied once.
+template <class Cloud>
+const double* positions_aos(const Cloud& cloud, std::vector<double>& tmp) {
+    using P = std::decay_t<decltype(cloud.positions[0])>;
+    const std::size_t n = cloud.positions.size();
+    if constexpr (std::is_same_v<P, std::array<double, 3>>) {
+        static_assert(sizeof(P) == 3 * sizeof(double), "std::array<double, 3> is padded");
+        return n ? cloud.positions[0].data() : nullptr;
+    } else {
+        tmp.resize(3 * n);
+        for (std::size_t i = 0; i < n; ++i)
+            for (int a = 0; a < 3; ++a) tmp[3 * i + a] = double(cloud.positions[i][a]);
+        return tmp.data();
+    }
 }
 
 template <class Row>
@@ -120,27 +171,37 @@ std::vector<Row> ledger(const kpme_gpu_config& c) {
 }  // namespace detail
 
 // kpme_apply (parallel.hpp:243-290). Result defaults to kpme_b200::KpmeResult;
-// pass kpme::KpmeResult to get the reference's own result type.
+// pass kpme::KpmeResult to get the reference's own result type. The one-shot
+// call reuses a cached plan for repeated configurations (kpme_gpu_apply).
 template <class Result = KpmeResult, class NumericalError = numerical_error, class Cfg,
           class Grid, class Dec, class Cloud, class Charges, class Opt>
 Result kpme_apply(const Cfg& cfg, const Grid& grid, int order, const Dec& dec, const Cloud& cloud,
-                  const Charges& q, const Opt& opt, const GpuOptions& gpu = {}) {
+                  const Charges& q, const Opt& opt, const GpuOptions& gpu = GpuOptions::from_env()) {
     if (dec.modes != cfg.modes)
         throw std::invalid_argument("kpme_apply: decomposition mode bound mismatch");
     const std::size_t n = cloud.positions.size();
     if (q.values.size() != n) throw std::invalid_argument("interpolate: charge count mismatch");
     const detail::Flat f = detail::flatten_dec(dec);
     const kpme_gpu_config c = detail::make_config(cfg, grid, order, dec, opt, f, gpu);
-    std::vector<double> xyz(3 * n);
-    for (std::size_t i = 0; i < n; ++i)
-        for (int a = 0; a < 3; ++a) xyz[3 * i + a] = cloud.positions[i][a];
+    std::vector<double> tmp;
+    const double* xyz = detail::positions_aos(cloud, tmp);
     Result r;
     r.potentials.assign(n, 0.0);
     throw_status<NumericalError>(
-        kpme_gpu_apply(&c, int64_t(n), xyz.data(), q.values.data(), r.potentials.data()));
+        kpme_gpu_apply(&c, int64_t(n), xyz, q.values.data(), r.potentials.data()));
     if (gpu.ledger)
         r.ledger = detail::ledger<typename std::decay_t<decltype(r.ledger)>::value_type>(c);
     return r;
+}
+
+// The reference's six-argument form (KpmeOptions defaulted, parallel.hpp:
+// 243-246): GPU options from the environment (GpuOptions::from_env).
+template <class Result = KpmeResult, class NumericalError = numerical_error, class Cfg,
+          class Grid, class Dec, class Cloud, class Charges>
+Result kpme_apply(const Cfg& cfg, const Grid& grid, int order, const Dec& dec, const Cloud& cloud,
+                  const Charges& q) {
+    return kpme_apply<Result, NumericalError>(cfg, grid, order, dec, cloud, q, DefaultOptions{},
+                                              GpuOptions::from_env());
 }
 
 // Steady-state plan: factor tables built once, device buffers reused.

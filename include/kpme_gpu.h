@@ -36,7 +36,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define KPME_GPU_ABI_VERSION 1
+#define KPME_GPU_ABI_VERSION 2
 
 /* Status codes. The C++ wrapper rethrows 1 as std::invalid_argument,
  * 2 as std::runtime_error and 3 as kpme::numerical_error, the exception
@@ -77,6 +77,12 @@ typedef struct {
     int threads;                /* KpmeOptions.threads (accepted, unused on GPU) */
     int device;                 /* CUDA device ordinal */
     int formulation;            /* KPME_GPU_FORM_* */
+    /* ABI 2: several devices driven by one process (a multi-device plan:
+     * z-slabs of whole cell planes, one per entry; see
+     * kpme_gpu_plan_create_multi for other rank grids). ndevices <= 1 uses
+     * `device` alone. */
+    int ndevices;
+    const int* devices;
 } kpme_gpu_config;
 
 typedef struct kpme_gpu_plan_s* kpme_gpu_plan;
@@ -112,9 +118,14 @@ int kpme_gpu_ledger(const kpme_gpu_config* cfg, int64_t* out, int64_t cap,
 
 /* ---- one-shot call ----------------------------------------------------- */
 /* kpme_apply (parallel.hpp:243-290) on host buffers: potentials[n] in
- * global particle order, including -c_Lambda * sum(q). */
+ * global particle order, including -c_Lambda * sum(q). Plans are cached per
+ * configuration (decomposition contents included) and device list, so
+ * repeated one-shot calls skip the factor build and the allocations;
+ * KPME_GPU_PLAN_CACHE=0 disables the cache. */
 int kpme_gpu_apply(const kpme_gpu_config* cfg, int64_t n, const double* xyz,
                    const double* q, double* potentials);
+/* Frees every cached plan of kpme_gpu_apply. */
+int kpme_gpu_apply_cache_clear(void);
 
 /* ---- plan API (steady state) ------------------------------------------- */
 /* Builds factor tables (W_a, the collapsed core G, dense A_a(lambda) when
@@ -180,6 +191,43 @@ int kpme_gpu_plan_forward(kpme_gpu_plan plan, int64_t n, const double* d_xyz,
 /* core (summed over slabs) -> backward contractions -> gather - c*sum(q) */
 int kpme_gpu_plan_backward(kpme_gpu_plan plan, const double* d_core,
                            double* d_potentials);
+
+/* ---- multi-device plans (one process drives several GPUs) --------------- */
+/* The reference's rank-grid decomposition of kpme_apply (RankGrid,
+ * parallel.hpp:46-82; SimulatedComm, parallel.hpp:98-145) on one node: a
+ * P0 x P1 x P2 grid of cell blocks, block r on cfg->devices[r] (ranks flatten
+ * like cells). Every device keeps its block's particles (routing on device),
+ * sorts, spreads and contracts them into a partial core; the partial cores
+ * are summed (the collapsed form's only exchange, replacing the axis-group
+ * reductions of spkmv, parallel.hpp:169-176, and allreduce_scalar,
+ * parallel.hpp:254-257); every device gathers its particles and the home
+ * device (devices[0]) returns all potentials in global order.
+ * kpme_gpu_plan_create with cfg->ndevices > 1 makes a (1, 1, ndevices) grid.
+ * execute and execute_device (buffers on the home device) and status work on
+ * a multi-device plan; the stage entry points, graphs and timing do not. */
+enum {
+    KPME_GPU_COLL_AUTO = 0, /* PEER when every device pair has peer access, else NCCL */
+    KPME_GPU_COLL_PEER = 1, /* each device sums all partial cores from peer memory
+                               (NVLink), in rank order: no NCCL round, same bits everywhere */
+    KPME_GPU_COLL_NCCL = 2  /* one grouped ncclAllReduce over the plan's own communicators */
+};
+int kpme_gpu_plan_create_multi(const kpme_gpu_config* cfg, int64_t max_particles,
+                               const int dims[3], kpme_gpu_plan* out);
+int kpme_gpu_plan_set_collective(kpme_gpu_plan plan, int mode);
+/* The exchange in use (KPME_GPU_COLL_*), or -1 for a single-device plan. */
+int kpme_gpu_plan_collective(kpme_gpu_plan plan);
+/* Device entries of the plan (count returned; up to cap written). */
+int kpme_gpu_plan_devices(kpme_gpu_plan plan, int* devices, int cap);
+
+/* ---- one process per GPU: a block plan owning an NCCL communicator ------ */
+/* Rank r of an nranks-process job (torchrun / MPI) builds its block plan
+ * (kpme_gpu_plan_create_slab/_block), rank 0 makes an id, the job broadcasts
+ * the 128 bytes, and every rank attaches. From then on execute_device and
+ * graph_execute run forward half -> ncclAllReduce of the core -> backward
+ * half on the plan's stream (capturable as one graph). */
+#define KPME_GPU_NCCL_ID_BYTES 128
+int kpme_gpu_nccl_unique_id(void* id);
+int kpme_gpu_plan_attach_comm(kpme_gpu_plan plan, int nranks, int rank, const void* id);
 
 /* ---- stage entry points (device buffers, plan stream) ------------------ */
 /* assign_particles (geometry.hpp:131-154), bit-exact: perm[n] is the

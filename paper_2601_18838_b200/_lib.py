@@ -13,6 +13,9 @@ LIB_PATH = os.path.join(HERE, "libkpme_b200.so")
 
 OK, INVALID_ARGUMENT, RUNTIME, NUMERICAL, CUDA, NCCL = range(6)
 FORM_AUTO, FORM_COLLAPSED, FORM_DENSE = 0, 1, 2
+COLL_AUTO, COLL_PEER, COLL_NCCL = 0, 1, 2
+NCCL_ID_BYTES = 128
+ABI_VERSION = 2
 DEFER_CHECKS = 1
 
 _dp = C.POINTER(C.c_double)
@@ -39,6 +42,8 @@ class Config(C.Structure):
         ("threads", C.c_int),
         ("device", C.c_int),
         ("formulation", C.c_int),
+        ("ndevices", C.c_int),
+        ("devices", C.POINTER(C.c_int)),
     ]
 
 
@@ -99,6 +104,14 @@ def _load():
         "kpme_gpu_plan_core_size": (C.c_int, [P]),
         "kpme_gpu_plan_forward": (C.c_int, [P, C.c_int64, P, P, P]),
         "kpme_gpu_plan_backward": (C.c_int, [P, P, P]),
+        "kpme_gpu_apply_cache_clear": (C.c_int, []),
+        "kpme_gpu_plan_create_multi": (C.c_int, [C.POINTER(Config), C.c_int64,
+                                                 C.POINTER(C.c_int), C.POINTER(P)]),
+        "kpme_gpu_plan_set_collective": (C.c_int, [P, C.c_int]),
+        "kpme_gpu_plan_collective": (C.c_int, [P]),
+        "kpme_gpu_plan_devices": (C.c_int, [P, C.POINTER(C.c_int), C.c_int]),
+        "kpme_gpu_nccl_unique_id": (C.c_int, [C.c_void_p]),
+        "kpme_gpu_plan_attach_comm": (C.c_int, [P, C.c_int, C.c_int, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -108,6 +121,9 @@ def _load():
 
 
 lib = _load()
+if lib.kpme_gpu_abi_version() != ABI_VERSION:
+    raise ImportError(f"{LIB_PATH}: ABI {lib.kpme_gpu_abi_version()}, expected {ABI_VERSION} "
+                      "(stale build; rerun __graft_entry__.build())")
 
 #: every function include/kpme_gpu.h declares (checked by tests/test_abi.py)
 EXPORTS = sorted(
@@ -123,6 +139,9 @@ EXPORTS = sorted(
         "kpme_gpu_plan_axis_operands", "kpme_gpu_dgemm_tn", "kpme_gpu_plan_create_slab",
         "kpme_gpu_plan_core_size", "kpme_gpu_plan_forward", "kpme_gpu_plan_backward",
         "kpme_gpu_plan_set_host_chunks", "kpme_gpu_plan_create_block",
+        "kpme_gpu_apply_cache_clear", "kpme_gpu_plan_create_multi",
+        "kpme_gpu_plan_set_collective", "kpme_gpu_plan_collective", "kpme_gpu_plan_devices",
+        "kpme_gpu_nccl_unique_id", "kpme_gpu_plan_attach_comm",
     ]
 )
 

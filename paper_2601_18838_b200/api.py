@@ -346,9 +346,11 @@ _FORMS = {"auto": _lib.FORM_AUTO, "collapsed": _lib.FORM_COLLAPSED, "dense": _li
 
 
 def make_config(cfg: EwaldConfig, grid: CellGrid, order: int, dec: SkpDecomposition,
-                opt: KpmeOptions | None = None, device: int = 0, formulation: str = "auto"):
+                opt: KpmeOptions | None = None, device: int = 0, formulation: str = "auto",
+                devices=None):
     """Marshal the reference's argument structs into kpme_gpu_config. Returns
-    (config, keep-alive arrays)."""
+    (config, keep-alive arrays). ``devices``: a device list (one process
+    driving several GPUs: a multi-device plan of z-slabs)."""
     opt = opt or KpmeOptions()
     w, prof = dec.arrays()
     keep = [np.ascontiguousarray(w if len(w) else np.zeros(1)),
@@ -366,17 +368,24 @@ def make_config(cfg: EwaldConfig, grid: CellGrid, order: int, dec: SkpDecomposit
     c.fuse_terms, c.threads = int(bool(opt.fuse_terms)), int(opt.threads)
     c.device = int(device)
     c.formulation = _FORMS[formulation]
+    if devices is not None and len(devices) > 1:
+        dv = (C.c_int * len(devices))(*[int(d) for d in devices])
+        keep.append(dv)
+        c.ndevices, c.devices = len(devices), C.cast(dv, C.POINTER(C.c_int))
+        c.device = int(devices[0])
     return c, keep
 
 
 def kpme_apply(cfg: EwaldConfig, grid: CellGrid, order: int, dec: SkpDecomposition,
                cloud: PointCloud, q: ChargeVector, opt: KpmeOptions | None = None, *,
-               device: int = 0, formulation: str = "auto") -> KpmeResult:
+               device: int = 0, formulation: str = "auto", devices=None) -> KpmeResult:
     """kpme_apply (parallel.hpp:243-290) on the GPU, host buffers in and out.
-    Raises ValueError where the reference throws std::invalid_argument."""
+    Raises ValueError where the reference throws std::invalid_argument.
+    ``devices`` (a list of ordinals) drives several GPUs from this process.
+    Plans are cached per configuration inside the library (kpme_gpu_apply)."""
     if dec.modes != cfg.modes:
         raise ValueError("kpme_apply: decomposition mode bound mismatch")
-    c, keep = make_config(cfg, grid, order, dec, opt, device, formulation)
+    c, keep = make_config(cfg, grid, order, dec, opt, device, formulation, devices)
     xyz = np.ascontiguousarray(cloud.positions, dtype=np.float64).reshape(-1, 3)
     qv = np.ascontiguousarray(q.values, dtype=np.float64)
     if qv.shape[0] != xyz.shape[0]:

@@ -259,14 +259,13 @@ void launch_factor_tables(const Geometry& g, int nterms, const double* tw, const
 void launch_core_forward(const Geometry& g, int S, const double* T1, const double* W0,
                          const double* W1, double* T2, const double* colq, double* F,
                          cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr_once;
+    once_per_device(attr_once, [&] {
         KB_CUDA(cudaFuncSetAttribute(k_core_a, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      200 * 1024));
         KB_CUDA(cudaFuncSetAttribute(k_core_c, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      200 * 1024));
-        attr = true;
-    }
+    });
     k_core_a<<<g.n[0], 128, sizeof(double) * 2 * g.n[1] * g.R, s>>>(g, S, T1, W1, T2);
     KB_CHECK_LAUNCH();
     k_core_b<<<dim3(g.R, (g.R * g.R + 31) / 32), 256, 0, s>>>(g, S, T2, W0, colq, F);
@@ -309,7 +308,7 @@ void launch_axis_operands(const Geometry& g, int a, int nterms, const double* W,
 
 void launch_cells_to_mesh(const Geometry& g, const double* src, double* dst, bool inverse,
                           cudaStream_t s) {
-    k_cells_mesh<<<148 * 8, 256, 0, s>>>(g, src, dst, inverse ? 1 : 0);
+    k_cells_mesh<<<sm_count() * 8, 256, 0, s>>>(g, src, dst, inverse ? 1 : 0);
     KB_CHECK_LAUNCH();
 }
 

@@ -205,7 +205,7 @@ int chunk_terms(int n0, int n1, int n2, int nterms) {
 int64_t tiles(int64_t M, int64_t N) { return ((M + BM - 1) / BM) * ((N + BN - 1) / BN); }
 int splits_for(int n0, int n1, int n2, int chunk) {
     const int64_t t = tiles((int64_t)n0 * n1, n2);
-    int s = (int)std::max<int64_t>(1, (2 * 148 + t - 1) / t);
+    int s = (int)std::max<int64_t>(1, (2 * sm_count() + t - 1) / t);
     return std::max(1, std::min(s, chunk));
 }
 
@@ -223,14 +223,13 @@ void dgemm_tn(cudaStream_t s, int64_t M, int64_t N, int64_t K, const double* in,
 void dgemm_tn_batched(cudaStream_t s, int64_t M, int64_t N, int64_t K, const double* in,
                       int64_t sin, const double* F, int64_t sF, double* out, int64_t sout,
                       int batch, bool accumulate) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr_once;
+    once_per_device(attr_once, [&] {
         KB_CUDA(cudaFuncSetAttribute(k_dgemm_tn<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kSmem));
         KB_CUDA(cudaFuncSetAttribute(k_dgemm_tn<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
-        attr = true;
-    }
+    });
     if (M <= 0 || N <= 0 || batch <= 0) return;
     const dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)batch);
     const bool vec = (M % 2 == 0) && (K % 2 == 0) && ((uintptr_t)in % 16 == 0) &&
@@ -278,7 +277,7 @@ void kron_matvec_dense(cudaStream_t s, int n0, int n1, int n2, int nterms, const
         // pass C over (term, z): y[(x',y')][z'] (+)= sum_{r,z} t2[r][z][(x',y')] C_r[z'][z]
         const int sp = even_splits(splits, cr);
         if (sp <= 1) {
-            k_concat_terms<<<148 * 4, 256, 0, s>>>(cr, n2, C + (int64_t)r0 * n2 * n2, ccat);
+            k_concat_terms<<<sm_count() * 4, 256, 0, s>>>(cr, n2, C + (int64_t)r0 * n2 * n2, ccat);
             KB_CHECK_LAUNCH();
             dgemm_tn(s, (int64_t)n0 * n1, n2, (int64_t)cr * n2, t2, ccat, y, r0 > 0);
         } else {
@@ -286,11 +285,11 @@ void kron_matvec_dense(cudaStream_t s, int n0, int n1, int n2, int nterms, const
             // [k tps, (k+1) tps) with its concatenated operand [z'][tps n2]
             // at ccat + k tps n2^2; partial sums summed in split order below
             const int tps = cr / sp;
-            k_concat_splits<<<148 * 4, 256, 0, s>>>(cr, tps, n2, C + (int64_t)r0 * n2 * n2, ccat);
+            k_concat_splits<<<sm_count() * 4, 256, 0, s>>>(cr, tps, n2, C + (int64_t)r0 * n2 * n2, ccat);
             KB_CHECK_LAUNCH();
             dgemm_tn_batched(s, (int64_t)n0 * n1, n2, (int64_t)tps * n2, t2, tps * mesh, ccat,
                              (int64_t)tps * n2 * n2, part, mesh, sp, false);
-            k_sum_splits<<<148 * 8, 256, 0, s>>>(mesh, sp, part, y, r0 > 0 ? 1 : 0);
+            k_sum_splits<<<sm_count() * 8, 256, 0, s>>>(mesh, sp, part, y, r0 > 0 ? 1 : 0);
             KB_CHECK_LAUNCH();
         }
     }

@@ -5,8 +5,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "kpme_gpu.h"
 
@@ -29,6 +31,43 @@ struct Error : std::runtime_error {
 
 #define KB_CHECK_LAUNCH() KB_CUDA(cudaGetLastError())
 
+// One-time setup per device (cudaFuncSetAttribute of kernels using more than
+// 48 KB of dynamic shared memory). Function attributes are per device, plans
+// may live on several devices of one process and be created from several
+// host threads, so a process-wide flag is not enough.
+struct PerDevice {
+    static constexpr int kMax = 64;
+    std::once_flag flag[kMax];
+};
+inline int current_device() {
+    int d = 0;
+    KB_CUDA(cudaGetDevice(&d));
+    if (d < 0 || d >= PerDevice::kMax) throw Error(KPME_GPU_CUDA, "device ordinal out of range");
+    return d;
+}
+template <class F>
+inline void once_per_device(PerDevice& pd, F&& f) {
+    std::call_once(pd.flag[current_device()], std::forward<F>(f));
+}
+// SM count of the current device (cached per device, thread-safe).
+int sm_count();
+
+// Makes `device` current for one ABI call and restores the caller's current
+// device afterwards (the reference API has no device state to disturb).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int device) {
+        KB_CUDA(cudaGetDevice(&prev));
+        if (prev != device) KB_CUDA(cudaSetDevice(device));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 #ifdef __CUDACC__
 // 256-bit global accesses (one LDG/STG.E.ENL2.256 per particle record on
 // sm_100a instead of two 128-bit ones: half the L2 requests for scattered
@@ -37,6 +76,22 @@ __device__ __forceinline__ void st_rec(double4* p, const double4& v) {
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z),
                  "d"(v.w)
                  : "memory");
+}
+// Cell index along one axis, bit-identical to the reference
+// (geometry.hpp:141-148): t = ((p - (c - r)) * K) / (2 r), floor, face
+// tie-break, clamp. The division is Markstein's correctly rounded quotient
+// q = RN(q0 + (a - b q0) y) with b = 2r, y = RN(1/b), q0 = RN(a y) (exact FMA
+// remainder), equal to RN(a / b) for these normal operands; the other
+// operations are explicit round-to-nearest (no FMA contraction). Shared by
+// every kernel that keys particles (sort, sort2, interp, route).
+__device__ __forceinline__ int exact_axis_cell(double p, double c, double r, int K, double b,
+                                               double y) {
+    const double a = __dmul_rn(__dsub_rn(p, __dsub_rn(c, r)), (double)K);
+    const double q0 = __dmul_rn(a, y);
+    const double t = __fma_rn(__fma_rn(-q0, b, a), y, q0);
+    int idx = (int)floor(t);
+    if (t == (double)idx && idx > 0) --idx;
+    return idx < 0 ? 0 : (idx > K - 1 ? K - 1 : idx);
 }
 __device__ __forceinline__ double4 ld_rec(const double4* p) {  // read-only data
     double4 v;

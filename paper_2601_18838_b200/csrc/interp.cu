@@ -24,16 +24,9 @@ __device__ __forceinline__ double cell_hi(const Geometry& g, int a, int i) {
     return g.center[a] - g.radius + 2.0 * g.radius * (i + 1) / g.K[a];
 }
 
-// Same exact key arithmetic as sort.cu (geometry.hpp:141-148), with the
-// correctly rounded (Markstein) division by 2r.
+// Same exact key arithmetic as the sort (internal.h, geometry.hpp:141-148).
 __device__ __forceinline__ int axis_cell(double p, double c, double r, int K, double y) {
-    const double b = __dmul_rn(2.0, r);
-    const double a = __dmul_rn(__dsub_rn(p, __dsub_rn(c, r)), (double)K);
-    const double q0 = __dmul_rn(a, y);
-    const double t = __fma_rn(__fma_rn(-q0, b, a), y, q0);
-    int idx = (int)floor(t);
-    if (t == (double)idx && idx > 0) --idx;
-    return idx < 0 ? 0 : (idx > K - 1 ? K - 1 : idx);
+    return exact_axis_cell(p, c, r, K, __dmul_rn(2.0, r), y);
 }
 
 // Equispaced Lagrange weights on [lo, hi] (lagrange_weights_1d,
@@ -1389,7 +1382,7 @@ size_t spread_smem(const Geometry& g) {
 int gather_batch(const Geometry& g, int S = 1) {
     const int L3 = g.L * g.L * g.L;
     const int seg = (g.z_hi - g.z_lo + S - 1) / std::max(1, S);
-    if (block_columns(g) * S <= 3 * 148 && seg <= kGatherTab && (size_t)seg * L3 * sizeof(double) <= 40 * 1024)
+    if (block_columns(g) * S <= 3 * sm_count() && seg <= kGatherTab && (size_t)seg * L3 * sizeof(double) <= 40 * 1024)
         return std::max(1, seg);
     const int cap = std::max(1, (GATHER_BATCH_KB * 1024) / (int)(sizeof(double) * L3));
     // equal batches for the same number of rounds: no short tail round
@@ -1405,12 +1398,11 @@ void launch_spread_mma_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
     const bool fits = spread_epilogue_doubles(L, R) <= SpreadTile<L>::stage;
     const size_t smem = sizeof(double) * (SpreadTile<L>::NW * spread_warp_doubles<L>(R) +
                                           (fits ? 0 : (size_t)spread_epilogue_doubles(L, R)));
-    static int attr_done = 0;
-    if (!attr_done) {
+    static PerDevice attr_once;
+    once_per_device(attr_once, [&] {
         KB_CUDA(cudaFuncSetAttribute(k_spread_mma<L, MONO>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_done = 1;
-    }
+    });
     if (smem > 200 * 1024) throw Error(KPME_GPU_INVALID_ARGUMENT, "spread: tile too large");
     const int grid = block_columns(a.g) * a.S;
     k_spread_mma<L, MONO><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
@@ -1423,14 +1415,13 @@ void launch_spread_mma_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
 template <int L>
 void launch_spread_uv_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
     const size_t smem = sizeof(double) * spread_uv_smem_doubles<L>(a.g.R, a.g.n[2]);
-    static int attr_done = 0;
-    if (!attr_done) {
+    static PerDevice attr_once;
+    once_per_device(attr_once, [&] {
         KB_CUDA(cudaFuncSetAttribute(k_spread_uv<L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      200 * 1024));
         KB_CUDA(cudaFuncSetAttribute(k_spread_uv<L, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      200 * 1024));
-        attr_done = 1;
-    }
+    });
     if (smem > 200 * 1024) {  // very long columns: the staged-product kernel
         launch_spread_mma_t<L, true>(a, want_fwd, s);
         return;
@@ -1462,12 +1453,11 @@ void launch_spread_mma(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
 
 template <int L, int MODE, bool MONO>
 void launch_gather_mode(const ColumnArgs& a, int grid, int cb, size_t smem, cudaStream_t s) {
-    static int attr_done = 0;
-    if (!attr_done) {
+    static PerDevice attr_once;
+    once_per_device(attr_once, [&] {
         KB_CUDA(cudaFuncSetAttribute(k_bwd_gather_t<L, MODE, MONO>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_done = 1;
-    }
+    });
     k_bwd_gather_t<L, MODE, MONO><<<grid, GT, smem, s>>>(a, cb);
 }
 
@@ -1506,14 +1496,13 @@ void launch_gather_t(const ColumnArgs& a0, int mode, cudaStream_t s) {
 }  // namespace
 
 void launch_spread_fwd(const ColumnArgs& a, int mode, bool want_fwd, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr_once;
+    once_per_device(attr_once, [&] {
         KB_CUDA(cudaFuncSetAttribute(k_spread_fwd<SPREAD_PARTICLES>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         KB_CUDA(cudaFuncSetAttribute(k_spread_fwd<SPREAD_FROM_CELLS>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
+    });
     if (mode == SPREAD_PARTICLES && a.g.L <= 8) {
         switch (a.g.L) {
             case 2: return launch_spread_mma<2>(a, want_fwd, s);
@@ -1535,16 +1524,15 @@ void launch_spread_fwd(const ColumnArgs& a, int mode, bool want_fwd, cudaStream_
 }
 
 void launch_bwd_gather(const ColumnArgs& a, int mode, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr_once;
+    once_per_device(attr_once, [&] {
         KB_CUDA(cudaFuncSetAttribute(k_bwd_gather<GATHER_FROM_B2>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         KB_CUDA(cudaFuncSetAttribute(k_bwd_gather<GATHER_FROM_CELLS>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         KB_CUDA(cudaFuncSetAttribute(k_bwd_gather<PSI_ONLY>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
+    });
     switch (a.g.L) {
         case 2: return launch_gather_t<2>(a, mode, s);
         case 3: return launch_gather_t<3>(a, mode, s);

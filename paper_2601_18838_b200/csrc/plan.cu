@@ -9,130 +9,40 @@
 //   backward z-expansion + gather - c*sum(q)        U_2 phase + anterpolate
 // The per-term loop of spkmv_sum is collapsed into the R^3 core G (core.cu).
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
-#include "internal.h"
-
-namespace kb {
-extern thread_local std::string g_last_error;
-}
+#include "plan.h"
 
 using kb::Error;
+using namespace kbp;
 
-// Particle chunks of the pipelined host path (kpme_gpu_plan_execute).
-constexpr int kMaxChunks = 8;
-
-struct kpme_gpu_plan_s {
-    kb::Geometry g{};
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    bool own_stream = false;
-    int64_t cap = 0;
-    int nterms = 0;
-    double correction = 0.0;
-    int S = 1;
-    int form = KPME_GPU_FORM_COLLAPSED;
-    int launches = 0;
-    int64_t last_n = 0;
-    bool use_sort2 = false;
-
-    // factor tables
-    double* tw = nullptr;
-    double* prof = nullptr;
-    double* W[3] = {nullptr, nullptr, nullptr};
-    double* WL[3] = {nullptr, nullptr, nullptr};  // W_a Lambda (monomial hot path)
-    double* lam = nullptr;
-    double4* cellax = nullptr;  // [K0 + K1 + K2] (lo, hi, mid, 1/half)
-    double* D = nullptr;
-    double* G = nullptr;
-    // collapsed-core work
-    double* T1 = nullptr;
-    double* T2 = nullptr;
-    double* F = nullptr;
-    double* B2 = nullptr;
-    double* colq = nullptr;
-    double* corr = nullptr;
-    double* Fpart = nullptr;
-    // sort
-    kb::SortBuffers sb{};
-    double4* sp = nullptr;
-    // host-buffer staging
-    double* xyz_d = nullptr;
-    double* q_d = nullptr;
-    double* out_d = nullptr;
-    unsigned long long* flags_h = nullptr;  // pinned
-    // chunked host path (kpme_gpu_plan_execute): copies on their own stream,
-    // one independent sort + spread per particle chunk
-    int host_chunks = -1;                   // -1: automatic
-    cudaStream_t cstream = nullptr;
-    cudaEvent_t ev_in[kMaxChunks] = {}, ev_out[kMaxChunks] = {};
-    int32_t* cstart = nullptr;              // [kMaxChunks][ncell + 1]
-    unsigned long long* cbad = nullptr;     // [kMaxChunks][2]
-    unsigned long long* cflags_h = nullptr; // pinned [kMaxChunks][2]
-    double* cFpart = nullptr;               // [R^3 + 1][kMaxChunks * S * ncol]
-    // dense form
-    double* A[3] = {nullptr, nullptr, nullptr};
-    double* cells = nullptr;
-    double* mesh_in = nullptr;
-    double* mesh_out = nullptr;
-    double* work = nullptr;
-    size_t work_bytes = 0;
-    // graph
-    cudaGraphExec_t gexec = nullptr;
-    int64_t g_n = -1;
-    const void* g_ptr[3] = {nullptr, nullptr, nullptr};
-    // timing
-    bool timing = false;
-    std::vector<cudaEvent_t> ev;
-    std::vector<double> stage_ms;
-    std::vector<void*> allocs;
-
-    template <class T>
-    T* alloc(size_t count) {
-        void* p = nullptr;
-        KB_CUDA(cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T)));
-        allocs.push_back(p);
-        return static_cast<T*>(p);
+int kb::sm_count() {
+    static std::atomic<int> cache[PerDevice::kMax];
+    const int d = current_device();
+    int v = cache[d].load(std::memory_order_relaxed);
+    if (!v) {
+        KB_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d));
+        cache[d].store(v, std::memory_order_relaxed);
     }
-    ~kpme_gpu_plan_s() {
-        cudaSetDevice(device);
-        if (gexec) cudaGraphExecDestroy(gexec);
-        for (int c = 0; c < kMaxChunks; ++c) {
-            if (ev_in[c]) cudaEventDestroy(ev_in[c]);
-            if (ev_out[c]) cudaEventDestroy(ev_out[c]);
-        }
-        if (cstream) cudaStreamDestroy(cstream);
-        if (cflags_h) cudaFreeHost(cflags_h);
-        for (auto e : ev) cudaEventDestroy(e);
-        for (void* p : allocs) cudaFree(p);
-        if (flags_h) cudaFreeHost(flags_h);
-        if (own_stream && stream) cudaStreamDestroy(stream);
-    }
-};
-
-namespace {
-
-template <class F>
-int guarded(F&& f) {
-    try {
-        f();
-        return KPME_GPU_OK;
-    } catch (const Error& e) {
-        kb::g_last_error = e.what();
-        return e.code;
-    } catch (const std::exception& e) {
-        kb::g_last_error = e.what();
-        return KPME_GPU_RUNTIME;
-    }
+    return v;
 }
 
-void invalid(const char* msg) { throw Error(KPME_GPU_INVALID_ARGUMENT, msg); }
+namespace kbp {
+
+// Entry points that work on one device's pipeline only.
+void need_single(kpme_gpu_plan p) {
+    if (!p) invalid("kpme_gpu: null plan");
+    if (p->multi)
+        invalid("kpme_gpu: not available on a multi-device plan (use execute / execute_device)");
+}
 
 // Argument checks of the reference constructors and kpme_apply.
 void validate(const kpme_gpu_config* c) {
@@ -271,6 +181,14 @@ void pipeline(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q, do
     }
     // spread + z, y, x forward contractions -> one partial core per column
     forward_core(p, a, p->F);
+    if (p->comm) {
+        // one rank of a multi-process job: sum the partial cores of all ranks
+        // (the collapsed form's only exchange) before the backward half
+        const ncclResult_t r = ncclAllReduce(p->F, p->F, (size_t)p->g.R * p->g.R * p->g.R + 1,
+                                             ncclDouble, ncclSum, p->comm, p->stream);
+        if (r != ncclSuccess)
+            throw Error(KPME_GPU_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+    }
     record(p, 3);
     // backward x, y, z expansions + gather - c sum(q), B2 rebuilt per column
     a.B2 = nullptr;
@@ -510,19 +428,92 @@ void collect_times(kpme_gpu_plan p) {
     }
 }
 
-}  // namespace
-
-namespace {
-void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, const int lo[3],
-                 const int hi[3], kpme_gpu_plan* out);
-}
+}  // namespace kbp
 
 extern "C" int kpme_gpu_plan_create(const kpme_gpu_config* cfg, int64_t max_particles,
                                     kpme_gpu_plan* out) {
     return guarded([&] {
         validate(cfg);
+        if (cfg->ndevices > 1) {
+            // z-slabs over the device list: the reference's (1, 1, G) rank grid
+            if (cfg->formulation == KPME_GPU_FORM_DENSE)
+                invalid("kpme_gpu: multi-device plans use the collapsed formulation");
+            const int dims[3] = {1, 1, cfg->ndevices};
+            create_multi(cfg, max_particles, dims, out);
+            return;
+        }
         const int lo[3] = {0, 0, 0}, hi[3] = {cfg->counts[0], cfg->counts[1], cfg->counts[2]};
         create_plan(cfg, max_particles, lo, hi, out);
+    });
+}
+
+extern "C" int kpme_gpu_plan_create_multi(const kpme_gpu_config* cfg, int64_t max_particles,
+                                          const int dims[3], kpme_gpu_plan* out) {
+    return guarded([&] {
+        validate(cfg);
+        if (!dims) invalid("kpme_gpu_plan_create_multi: null dims");
+        if (cfg->formulation == KPME_GPU_FORM_DENSE)
+            invalid("kpme_gpu: multi-device plans use the collapsed formulation");
+        create_multi(cfg, max_particles, dims, out);
+    });
+}
+
+extern "C" int kpme_gpu_plan_set_collective(kpme_gpu_plan p, int mode) {
+    return guarded([&] {
+        if (!p) invalid("kpme_gpu: null plan");
+        if (!p->multi) invalid("kpme_gpu_plan_set_collective: not a multi-device plan");
+        multi_set_collective(p, mode);
+    });
+}
+
+extern "C" int kpme_gpu_plan_collective(kpme_gpu_plan p) {
+    return p && p->multi ? multi_collective(p) : -1;
+}
+
+extern "C" int kpme_gpu_plan_devices(kpme_gpu_plan p, int* devices, int cap) {
+    if (!p) return -1;
+    std::vector<int> d = multi_devices(p);
+    for (int i = 0; i < (int)d.size() && i < cap; ++i) devices[i] = d[i];
+    return (int)d.size();
+}
+
+extern "C" int kpme_gpu_nccl_unique_id(void* id) {
+    return guarded([&] {
+        if (!id) invalid("kpme_gpu_nccl_unique_id: null id");
+        static_assert(sizeof(ncclUniqueId) == KPME_GPU_NCCL_ID_BYTES, "ncclUniqueId size");
+        ncclUniqueId u;
+        const ncclResult_t r = ncclGetUniqueId(&u);
+        if (r != ncclSuccess)
+            throw Error(KPME_GPU_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+        std::memcpy(id, &u, sizeof(u));
+    });
+}
+
+extern "C" int kpme_gpu_plan_attach_comm(kpme_gpu_plan p, int nranks, int rank, const void* id) {
+    return guarded([&] {
+        if (!p) invalid("kpme_gpu: null plan");
+        if (p->multi) invalid("kpme_gpu_plan_attach_comm: multi-device plans own their exchange");
+        if (!id || nranks < 1 || rank < 0 || rank >= nranks)
+            invalid("kpme_gpu_plan_attach_comm: bad rank / id");
+        if (p->form == KPME_GPU_FORM_DENSE)
+            invalid("kpme_gpu_plan_attach_comm: the dense formulation has no core exchange");
+        const kb::DeviceGuard dg(p->device);
+        if (p->gexec) {
+            KB_CUDA(cudaGraphExecDestroy(p->gexec));
+            p->gexec = nullptr;
+        }
+        if (p->comm) {
+            ncclCommDestroy(p->comm);
+            p->comm = nullptr;
+        }
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof(u));
+        const ncclResult_t r = ncclCommInitRank(&p->comm, nranks, u, rank);
+        if (r != ncclSuccess) {
+            p->comm = nullptr;
+            throw Error(KPME_GPU_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        }
+        p->comm_ranks = nranks;
     });
 }
 
@@ -556,21 +547,21 @@ extern "C" int kpme_gpu_plan_core_size(kpme_gpu_plan p) {
 extern "C" int kpme_gpu_plan_forward(kpme_gpu_plan p, int64_t n, const double* xyz,
                                      const double* q, double* core) {
     return guarded([&] {
-        if (!p) invalid("kpme_gpu: null plan");
-        KB_CUDA(cudaSetDevice(p->device));
+        need_single(p);
+        const kb::DeviceGuard dg(p->device);
         forward_half(p, n, xyz, q, core);
     });
 }
 
 extern "C" int kpme_gpu_plan_backward(kpme_gpu_plan p, const double* core, double* out) {
     return guarded([&] {
-        if (!p) invalid("kpme_gpu: null plan");
-        KB_CUDA(cudaSetDevice(p->device));
+        need_single(p);
+        const kb::DeviceGuard dg(p->device);
         backward_half(p, core, out);
     });
 }
 
-namespace {
+namespace kbp {
 void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, const int lo[3],
                  const int hi[3], kpme_gpu_plan* out) {
     {
@@ -581,7 +572,7 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, const int lo
         auto p = new kpme_gpu_plan_s();
         try {
             p->device = cfg->device;
-            KB_CUDA(cudaSetDevice(p->device));
+            const kb::DeviceGuard dg(p->device);
             KB_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
             p->own_stream = true;
             kb::Geometry& g = p->g;
@@ -619,7 +610,7 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, const int lo
             // z segments per column: enough CTAs for one resident wave (3 per SM
             // for the column kernels), never more than one wave
             p->S = std::max(1, std::min(std::max(1, g.z_hi - g.z_lo),
-                                        (3 * 148) / std::max(1, kb::block_columns(g))));
+                                        (3 * kb::sm_count()) / std::max(1, kb::block_columns(g))));
 #endif
 
             const int P = 2 * g.M + 1;
@@ -734,7 +725,7 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, const int lo
         }
     }
 }
-}  // namespace
+}  // namespace kbp
 
 extern "C" int kpme_gpu_plan_destroy(kpme_gpu_plan plan) {
     return guarded([&] { delete plan; });
@@ -743,6 +734,11 @@ extern "C" int kpme_gpu_plan_destroy(kpme_gpu_plan plan) {
 extern "C" int kpme_gpu_plan_set_stream(kpme_gpu_plan p, void* stream) {
     return guarded([&] {
         if (!p) invalid("kpme_gpu: null plan");
+        if (p->multi) {
+            // the home device's part runs the caller-facing stream
+            multi_set_home_stream(p, static_cast<cudaStream_t>(stream));
+            return;
+        }
         if (p->gexec) {
             cudaGraphExecDestroy(p->gexec);
             p->gexec = nullptr;
@@ -757,7 +753,11 @@ extern "C" int kpme_gpu_plan_execute_device(kpme_gpu_plan p, int64_t n, const do
                                             const double* q, double* out, int flags) {
     return guarded([&] {
         if (!p) invalid("kpme_gpu: null plan");
-        KB_CUDA(cudaSetDevice(p->device));
+        if (p->multi) {
+            multi_execute_device(p, n, xyz, q, out, flags);
+            return;
+        }
+        const kb::DeviceGuard dg(p->device);
         pipeline(p, n, xyz, q, out);
         collect_times(p);
         if (!(flags & KPME_GPU_DEFER_CHECKS)) sync_and_check(p);
@@ -767,7 +767,11 @@ extern "C" int kpme_gpu_plan_execute_device(kpme_gpu_plan p, int64_t n, const do
 extern "C" int kpme_gpu_plan_status(kpme_gpu_plan p) {
     return guarded([&] {
         if (!p) invalid("kpme_gpu: null plan");
-        KB_CUDA(cudaSetDevice(p->device));
+        if (p->multi) {
+            multi_status(p);
+            return;
+        }
+        const kb::DeviceGuard dg(p->device);
         sync_and_check(p);
     });
 }
@@ -776,8 +780,12 @@ extern "C" int kpme_gpu_plan_execute(kpme_gpu_plan p, int64_t n, const double* x
                                      const double* q, double* out) {
     return guarded([&] {
         if (!p) invalid("kpme_gpu: null plan");
+        if (p->multi) {
+            multi_execute_host(p, n, xyz, q, out);
+            return;
+        }
         if (n > p->cap) invalid("kpme_gpu: more particles than the plan was created for");
-        KB_CUDA(cudaSetDevice(p->device));
+        const kb::DeviceGuard dg(p->device);
         const int C = chunk_count(p, n);
         ensure_host_buffers(p, C > 1);
         if (C > 1 && !p->timing) {
@@ -810,8 +818,8 @@ extern "C" int kpme_gpu_plan_set_host_chunks(kpme_gpu_plan p, int chunks) {
 extern "C" int kpme_gpu_plan_graph_execute(kpme_gpu_plan p, int64_t n, const double* xyz,
                                            const double* q, double* out) {
     return guarded([&] {
-        if (!p) invalid("kpme_gpu: null plan");
-        KB_CUDA(cudaSetDevice(p->device));
+        need_single(p);
+        const kb::DeviceGuard dg(p->device);
         const bool same = p->gexec && p->g_n == n && p->g_ptr[0] == xyz && p->g_ptr[1] == q &&
                           p->g_ptr[2] == out;
         if (!same) {
@@ -849,8 +857,8 @@ extern "C" int kpme_gpu_plan_launches(kpme_gpu_plan p) { return p ? p->launches 
 
 extern "C" int kpme_gpu_plan_enable_timing(kpme_gpu_plan p, int on) {
     return guarded([&] {
-        if (!p) invalid("kpme_gpu: null plan");
-        KB_CUDA(cudaSetDevice(p->device));
+        need_single(p);
+        const kb::DeviceGuard dg(p->device);
         if (on && p->ev.empty()) {
             p->ev.resize(5);
             for (auto& e : p->ev) KB_CUDA(cudaEventCreate(&e));
@@ -861,22 +869,163 @@ extern "C" int kpme_gpu_plan_enable_timing(kpme_gpu_plan p, int on) {
 
 extern "C" int kpme_gpu_plan_stage_times(kpme_gpu_plan p, double* ms, int cap, int* count) {
     return guarded([&] {
-        if (!p) invalid("kpme_gpu: null plan");
+        need_single(p);
         const int c = (int)p->stage_ms.size();
         for (int i = 0; i < c && i < cap; ++i) ms[i] = p->stage_ms[i];
         *count = c;
     });
 }
 
+// ---- one-shot kpme_gpu_apply with a plan cache --------------------------------
+//
+// The reference's kpme_apply is a pure function of its arguments; building a
+// plan (factor tables, G, allocations) costs far more than one apply at small
+// N, so plans are kept per configuration. The key holds every field of the
+// config and the full decomposition, so a cached plan is exactly the plan a
+// fresh call would build. A plan in use by one thread is invisible to others.
+
+namespace {
+struct CacheEntry {
+    std::string key;
+    kpme_gpu_plan plan = nullptr;
+    int64_t cap = 0;
+    bool busy = false;
+    uint64_t used = 0;
+};
+constexpr size_t kCacheEntries = 4;
+std::mutex g_cache_mu;
+std::vector<CacheEntry>* g_cache = new std::vector<CacheEntry>();  // leaked: outlives CUDA teardown
+uint64_t g_tick = 0;
+
+bool cache_on() {
+    static const bool on = [] {
+        const char* e = getenv("KPME_GPU_PLAN_CACHE");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
+template <class T>
+void put(std::string& k, const T& v) {
+    k.append(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+
+std::string config_key(const kpme_gpu_config* c) {
+    std::string k;
+    put(k, c->xi);
+    put(k, c->modes);
+    for (int a = 0; a < 3; ++a) put(k, c->center[a]);
+    put(k, c->radius);
+    for (int a = 0; a < 3; ++a) put(k, c->counts[a]);
+    put(k, c->order);
+    put(k, c->dec_modes);
+    put(k, c->correction);
+    put(k, c->nterms);
+    put(k, c->formulation);
+    const int nd = c->ndevices > 1 ? c->ndevices : 0;
+    put(k, nd);
+    if (nd)
+        for (int d = 0; d < nd; ++d) put(k, c->devices[d]);
+    else
+        put(k, c->device);
+    const size_t P = 2 * (size_t)c->modes + 1;
+    if (c->nterms > 0) {
+        k.append(reinterpret_cast<const char*>(c->term_weights), sizeof(double) * c->nterms);
+        k.append(reinterpret_cast<const char*>(c->profiles), sizeof(double) * c->nterms * 3 * P);
+    }
+    return k;
+}
+}  // namespace
+
+extern "C" int kpme_gpu_apply_cache_clear(void) {
+    std::vector<CacheEntry> drop;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        std::vector<CacheEntry> keep;
+        for (auto& e : *g_cache) (e.busy ? keep : drop).push_back(e);
+        g_cache->swap(keep);
+    }
+    for (auto& e : drop) kpme_gpu_plan_destroy(e.plan);
+    return KPME_GPU_OK;
+}
+
 extern "C" int kpme_gpu_apply(const kpme_gpu_config* cfg, int64_t n, const double* xyz,
                               const double* q, double* potentials) {
-    kpme_gpu_plan p = nullptr;
-    int st = kpme_gpu_plan_create(cfg, n, &p);
+    if (!cache_on()) {
+        kpme_gpu_plan p = nullptr;
+        int st = kpme_gpu_plan_create(cfg, n, &p);
+        if (st) return st;
+        st = kpme_gpu_plan_execute(p, n, xyz, q, potentials);
+        const std::string keep = kb::g_last_error;
+        kpme_gpu_plan_destroy(p);
+        kb::g_last_error = keep;
+        return st;
+    }
+    std::string key;
+    int st = guarded([&] {
+        validate(cfg);
+        if (n < 0) invalid("kpme_gpu_apply: negative particle count");
+        key = config_key(cfg);
+    });
     if (st) return st;
+    kpme_gpu_plan p = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (auto& e : *g_cache)
+            if (!e.busy && e.key == key && e.cap >= n) {
+                e.busy = true;
+                e.used = ++g_tick;
+                p = e.plan;
+                break;
+            }
+    }
+    const bool fresh = p == nullptr;
+    if (fresh) {
+        st = kpme_gpu_plan_create(cfg, std::max<int64_t>(n, 1), &p);
+        if (st) return st;
+    }
     st = kpme_gpu_plan_execute(p, n, xyz, q, potentials);
-    const std::string keep = kb::g_last_error;
-    kpme_gpu_plan_destroy(p);
-    kb::g_last_error = keep;
+    const std::string err = kb::g_last_error;
+    // an argument error leaves the plan reusable (every execute resets its
+    // flags); anything else retires it
+    const bool reusable = st == KPME_GPU_OK || st == KPME_GPU_INVALID_ARGUMENT;
+    std::vector<kpme_gpu_plan> drop;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        if (fresh) {
+            if (reusable) {
+                CacheEntry e;
+                e.key = key;
+                e.plan = p;
+                e.cap = std::max<int64_t>(n, 1);
+                e.used = ++g_tick;
+                g_cache->push_back(e);
+            } else {
+                drop.push_back(p);
+            }
+        } else {
+            for (size_t i = 0; i < g_cache->size(); ++i)
+                if ((*g_cache)[i].plan == p) {
+                    (*g_cache)[i].busy = false;
+                    if (!reusable) {
+                        drop.push_back(p);
+                        g_cache->erase(g_cache->begin() + i);
+                    }
+                    break;
+                }
+        }
+        while (g_cache->size() > kCacheEntries) {  // least recently used idle plan
+            int lru = -1;
+            for (size_t i = 0; i < g_cache->size(); ++i)
+                if (!(*g_cache)[i].busy && (lru < 0 || (*g_cache)[i].used < (*g_cache)[lru].used))
+                    lru = (int)i;
+            if (lru < 0) break;
+            drop.push_back((*g_cache)[lru].plan);
+            g_cache->erase(g_cache->begin() + lru);
+        }
+    }
+    for (auto d : drop) kpme_gpu_plan_destroy(d);
+    kb::g_last_error = err;
     return st;
 }
 
@@ -885,9 +1034,9 @@ extern "C" int kpme_gpu_apply(const kpme_gpu_config* cfg, int64_t n, const doubl
 extern "C" int kpme_gpu_sort(kpme_gpu_plan p, int64_t n, const double* xyz, int32_t* perm,
                              int32_t* cell_start) {
     return guarded([&] {
-        if (!p) invalid("kpme_gpu: null plan");
+        need_single(p);
         if (n > p->cap) invalid("kpme_gpu: more particles than the plan was created for");
-        KB_CUDA(cudaSetDevice(p->device));
+        const kb::DeviceGuard dg(p->device);
         reset_flags(p);
         sort_and_permute(p, n, xyz, nullptr);
         if (n > 0)
@@ -902,9 +1051,9 @@ extern "C" int kpme_gpu_sort(kpme_gpu_plan p, int64_t n, const double* xyz, int3
 extern "C" int kpme_gpu_spread(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q,
                                double* phi_cells) {
     return guarded([&] {
-        if (!p) invalid("kpme_gpu: null plan");
+        need_single(p);
         if (n > p->cap) invalid("kpme_gpu: more particles than the plan was created for");
-        KB_CUDA(cudaSetDevice(p->device));
+        const kb::DeviceGuard dg(p->device);
         reset_flags(p);
         sort_and_permute(p, n, xyz, q);
         kb::ColumnArgs a = column_args(p);
@@ -916,8 +1065,8 @@ extern "C" int kpme_gpu_spread(kpme_gpu_plan p, int64_t n, const double* xyz, co
 
 extern "C" int kpme_gpu_skp_apply(kpme_gpu_plan p, const double* phi_cells, double* psi_cells) {
     return guarded([&] {
-        if (!p) invalid("kpme_gpu: null plan");
-        KB_CUDA(cudaSetDevice(p->device));
+        need_single(p);
+        const kb::DeviceGuard dg(p->device);
         if (p->form == KPME_GPU_FORM_DENSE) {
             kb::launch_cells_to_mesh(p->g, phi_cells, p->mesh_in, false, p->stream);
             kb::kron_matvec_dense(p->stream, p->g.n[0], p->g.n[1], p->g.n[2], p->nterms, p->A[0],
@@ -945,9 +1094,9 @@ extern "C" int kpme_gpu_skp_apply(kpme_gpu_plan p, const double* phi_cells, doub
 extern "C" int kpme_gpu_gather(kpme_gpu_plan p, int64_t n, const double* xyz,
                                const double* psi_cells, double* out) {
     return guarded([&] {
-        if (!p) invalid("kpme_gpu: null plan");
+        need_single(p);
         if (n > p->cap) invalid("kpme_gpu: more particles than the plan was created for");
-        KB_CUDA(cudaSetDevice(p->device));
+        const kb::DeviceGuard dg(p->device);
         reset_flags(p);
         // the permute needs charges; gather ignores them, pass positions twice
         sort_and_permute(p, n, xyz, nullptr);
@@ -963,9 +1112,9 @@ extern "C" int kpme_gpu_gather(kpme_gpu_plan p, int64_t n, const double* xyz,
 
 extern "C" int kpme_gpu_plan_axis_operands(kpme_gpu_plan p, int axis, double* out) {
     return guarded([&] {
-        if (!p) invalid("kpme_gpu: null plan");
+        need_single(p);
         if (axis < 0 || axis > 2) invalid("kpme_gpu_plan_axis_operands: bad axis");
-        KB_CUDA(cudaSetDevice(p->device));
+        const kb::DeviceGuard dg(p->device);
         kb::launch_axis_operands(p->g, axis, p->nterms, p->W[axis], p->D, out, p->stream);
         KB_CUDA(cudaStreamSynchronize(p->stream));
     });
@@ -983,7 +1132,7 @@ extern "C" int kpme_gpu_kron_matvec_dense(int device, void* stream, int n0, int 
                                           void* work, size_t work_bytes) {
     return guarded([&] {
         if (n0 < 1 || n1 < 1 || n2 < 1 || nterms < 0) invalid("kron_matvec_dense: bad shape");
-        KB_CUDA(cudaSetDevice(device));
+        const kb::DeviceGuard dg(device);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         void* w = work;
         size_t wb = work_bytes;

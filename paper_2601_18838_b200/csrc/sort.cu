@@ -22,22 +22,9 @@ constexpr int kRankCap = 256;      // warp rank-count sort
 constexpr int kWarpCap = 512;      // warp bitonic sort of (index, slot) pairs
 constexpr int kBlockCap = 16384;   // CTA bitonic sort in shared memory
 
-// Cell index along one axis, bit-identical to the reference
-// (geometry.hpp:141-148): t = ((p - (c - r)) * K) / (2 r), floor, face
-// tie-break, clamp. The division is Markstein's correctly rounded quotient
-// q = RN(q0 + (a - b q0) y) with y = RN(1/b), q0 = RN(a y) (exact FMA
-// remainder), equal to RN(a / b) for these normal operands; the other
-// operations are explicit round-to-nearest (no FMA contraction).
 __device__ __forceinline__ int axis_cell(double p, double c, double r, int K, double b,
                                          double y) {
-    const double a = __dmul_rn(__dsub_rn(p, __dsub_rn(c, r)), (double)K);
-    const double q0 = __dmul_rn(a, y);
-    const double t = __fma_rn(__fma_rn(-q0, b, a), y, q0);
-    int idx = (int)floor(t);
-    if (t == (double)idx && idx > 0) --idx;
-    if (idx < 0) idx = 0;
-    if (idx > K - 1) idx = K - 1;
-    return idx;
+    return exact_axis_cell(p, c, r, K, b, y);
 }
 
 __global__ void __launch_bounds__(256) k_keys(Geometry g, int64_t n, const double* __restrict__ xyz,
@@ -327,12 +314,11 @@ int blocks_for(int64_t n, int threads) { return (int)((n + threads - 1) / thread
 void launch_sort(const Geometry& g, int64_t n, const double* xyz, const SortBuffers& b,
                  cudaStream_t s, int* launches, const double* q, double4* sp) {
     if (!q) sp = nullptr;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static PerDevice attr_once;
+    once_per_device(attr_once, [&] {
         KB_CUDA(cudaFuncSetAttribute(k_segsort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kBlockCap * (int)sizeof(unsigned long long)));
-        attr_set = true;
-    }
+    });
     KB_CUDA(cudaMemsetAsync(b.cnt, 0, sizeof(int32_t) * g.ncell, s));
     KB_CUDA(cudaMemsetAsync(b.nbig, 0, sizeof(int32_t), s));
     if (n > 0) {
@@ -349,7 +335,7 @@ void launch_sort(const Geometry& g, int64_t n, const double* xyz, const SortBuff
         k_segsort_warp<<<(g.ncell + 7) / 8, 256, 0, s>>>(g.ncell, b.start, b.perm, b.big, b.nbig,
                                                          b.rec, sp);
         KB_CHECK_LAUNCH();
-        k_segsort_big<<<148, 1024, kBlockCap * sizeof(unsigned long long), s>>>(
+        k_segsort_big<<<sm_count(), 1024, kBlockCap * sizeof(unsigned long long), s>>>(
             n, b.key, b.start, b.perm, b.big, b.nbig, b.rec, sp, xyz, q);
         KB_CHECK_LAUNCH();
         l += 4;
@@ -361,7 +347,7 @@ void launch_permute(int64_t n, const double* xyz, const double* q, const int32_t
                     double4* sp, cudaStream_t s) {
     if (n <= 0) return;
     const int64_t blk = (n + 255) / 256;
-    k_permute<<<(int)(blk > 148 * 16 ? 148 * 16 : blk), 256, 0, s>>>(n, xyz, q, perm, sp);
+    k_permute<<<(int)(blk > sm_count() * 16 ? sm_count() * 16 : blk), 256, 0, s>>>(n, xyz, q, perm, sp);
     KB_CHECK_LAUNCH();
 }
 

@@ -45,17 +45,10 @@ constexpr int kZRounds = SORT2_ZROUNDS;
 constexpr int kZChunk = kZWarps * kZRounds * 32;  // column elements staged per chunk
 static_assert(kRounds % kGroup == 0, "rounds come in load groups");
 
-// Markstein-division axis cell, identical to sort.cu's axis_cell:
+// Markstein-division axis cell (internal.h):
 __device__ __forceinline__ int axis_cell2(double p, double c, double r, int K, double b,
                                           double y) {
-    const double a = __dmul_rn(__dsub_rn(p, __dsub_rn(c, r)), (double)K);
-    const double q0 = __dmul_rn(a, y);
-    const double t = __fma_rn(__fma_rn(-q0, b, a), y, q0);
-    int idx = (int)floor(t);
-    if (t == (double)idx && idx > 0) --idx;
-    if (idx < 0) idx = 0;
-    if (idx > K - 1) idx = K - 1;
-    return idx;
+    return exact_axis_cell(p, c, r, K, b, y);
 }
 
 // Lanes of the warp holding the same non-negative key (inactive lanes pass a
@@ -1004,11 +997,10 @@ size_t sort2_hist_entries(const Geometry& g, int64_t cap) {  // also the tile pa
 // (308 vs 234 us). KPME_SORT_TILES=0 / 1 forces the column scatter / the tile
 // path wherever it fits (tests, A/B).
 static bool tiles_chosen(int ncol) {
-    static int m = -1;
-    if (m < 0) {
+    static const int m = [] {
         const char* e = getenv("KPME_SORT_TILES");
-        m = (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 1 : 2;
-    }
+        return (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 1 : 2;
+    }();
     return m == 1 || (m == 2 && ncol * 4 <= kTile);
 }
 
@@ -1028,13 +1020,7 @@ static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, 
     // Tile rounds: the fewest (waves x tile length) at two CTAs per SM, among
     // tiles holding >= 4 particles per column on average (the pieces k_z_tiles
     // gathers); ties go to the longer tile. Config 3: 559 tiles of 1792.
-    static int slots = 0;
-    if (!slots) {
-        int dev = 0, sms = 0;
-        KB_CUDA(cudaGetDevice(&dev));
-        KB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        slots = 2 * sms;
-    }
+    const int slots = 2 * sm_count();
     int tr = 8;
     {
         int64_t best = -1;
@@ -1056,8 +1042,8 @@ static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, 
     const ZTilesLayout ZL(g.K[2], ntiles, wcap);
     if (TL.total > kTileMaxSmem || ntiles > 65535 || ZL.total_chunked > 160 * 1024) return false;
     const int cb = (bits_for(ncol) + 1) & ~1, zb = (bits_for(g.K[2]) + 1) & ~1;
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr_once;
+    once_per_device(attr_once, [&] {
         for (int bb = 2; bb <= 16; bb += 2) {
             for (int r : {4, 7, 8})
                 KB_CUDA(cudaFuncSetAttribute(pick_bits(bb, [r](auto B) {
@@ -1069,8 +1055,7 @@ static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, 
             KB_CUDA(cudaFuncSetAttribute(pick_bits(bb, [](auto B) { return &k_z_tiles<decltype(B)::value>; }),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
         }
-        attr = true;
-    }
+    });
     auto tile_kernel = pick_bits(cb, [tr](auto B) {
         return pick_rounds(tr, [](auto T) { return &k_tile_sort<decltype(B)::value, decltype(T)::value>; });
     });
@@ -1102,8 +1087,8 @@ void launch_sort2(const Geometry& g, int64_t n, const double* xyz, const SortBuf
     const int cb = (bits_for(ncol) + 1) & ~1, zb = (bits_for(g.K[2]) + 1) & ~1;
     auto col_kernel = pick_bits(cb, [](auto B) { return &k_col_scatter<decltype(B)::value>; });
     auto z_kernel = pick_bits(zb, [](auto B) { return &k_z_sort<decltype(B)::value>; });
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr_once;
+    once_per_device(attr_once, [&] {
         for (int b = 2; b <= 16; b += 2) {
             KB_CUDA(cudaFuncSetAttribute(pick_bits(b, [](auto B) { return &k_col_scatter<decltype(B)::value>; }),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
@@ -1112,8 +1097,7 @@ void launch_sort2(const Geometry& g, int64_t n, const double* xyz, const SortBuf
         }
         KB_CUDA(cudaFuncSetAttribute(k_tile_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      160 * 1024));
-        attr = true;
-    }
+    });
     const int ntiles = (int)std::max<int64_t>(1, (n + kTile - 1) / kTile);
     const int64_t E = (int64_t)ncol * ntiles;
     int l = 0;

@@ -152,6 +152,17 @@ class KpmePlan:
         self._leave()
         return out
 
+    def attach_comm(self, nranks: int, rank: int, uid: bytes):
+        """Own an NCCL communicator (rank ``rank`` of ``nranks``; ``uid`` from
+        ``nccl_unique_id()`` on rank 0, broadcast by the job). Afterwards
+        ``execute``/``execute_graph`` sum the partial cores of all ranks
+        inside the library: forward half -> ncclAllReduce -> backward half."""
+        if len(uid) != _lib.NCCL_ID_BYTES:
+            raise ValueError("kpme_gpu: NCCL unique id must be 128 bytes")
+        buf = C.create_string_buffer(bytes(uid), _lib.NCCL_ID_BYTES)
+        with torch.cuda.device(self.device):
+            check(lib.kpme_gpu_plan_attach_comm(self._h, int(nranks), int(rank), buf))
+
     def status(self):
         check(lib.kpme_gpu_plan_status(self._h))
 
@@ -212,6 +223,96 @@ class KpmePlan:
         check(lib.kpme_gpu_plan_axis_operands(self._h, axis, _ptr(out)))
         self._leave()
         return out[: len(self.dec.terms)]
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (128 bytes)."""
+    buf = C.create_string_buffer(_lib.NCCL_ID_BYTES)
+    check(lib.kpme_gpu_nccl_unique_id(buf))
+    return buf.raw
+
+
+class MultiDevicePlan:
+    """One process driving several GPUs (kpme_gpu_plan_create_multi): a
+    P0 x P1 x P2 grid of cell blocks, block r on ``devices[r]`` (RankGrid,
+    parallel.hpp:46-82). Inputs and outputs live on the home device
+    ``devices[0]`` (or on the host for ``execute_host``); the partial cores
+    are summed from peer memory (``collective="peer"``) or by NCCL."""
+
+    _COLL = {"auto": _lib.COLL_AUTO, "peer": _lib.COLL_PEER, "nccl": _lib.COLL_NCCL}
+
+    def __init__(self, cfg: EwaldConfig, grid: CellGrid, order: int, dec: SkpDecomposition,
+                 max_particles: int, devices, dims=None, opt: KpmeOptions | None = None,
+                 collective: str = "auto"):
+        devices = [int(d) for d in devices]
+        self.cfg, self.grid, self.order, self.dec = cfg, grid, order, dec
+        self.devices = devices
+        self.device = devices[0]
+        self.dims = tuple(dims) if dims is not None else (1, 1, len(devices))
+        self._c, self._keep = make_config(cfg, grid, order, dec, opt, devices[0], "collapsed")
+        dv = (C.c_int * len(devices))(*devices)
+        self._keep.append(dv)
+        self._c.ndevices, self._c.devices = len(devices), C.cast(dv, C.POINTER(C.c_int))
+        self._h = C.c_void_p()
+        d3 = (C.c_int * 3)(*self.dims)
+        with torch.cuda.device(self.device):
+            check(lib.kpme_gpu_plan_create_multi(C.byref(self._c), int(max_particles), d3,
+                                                 C.byref(self._h)))
+        if collective != "auto":
+            self.set_collective(collective)
+        self.stream = torch.cuda.Stream(device=self.device)
+        check(lib.kpme_gpu_plan_set_stream(self._h, C.c_void_p(self.stream.cuda_stream)))
+
+    def set_collective(self, mode: str):
+        check(lib.kpme_gpu_plan_set_collective(self._h, self._COLL[mode]))
+
+    @property
+    def collective(self) -> str:
+        return {v: k for k, v in self._COLL.items()}[lib.kpme_gpu_plan_collective(self._h)]
+
+    def execute(self, xyz: torch.Tensor, q: torch.Tensor, out: torch.Tensor | None = None,
+                defer_checks: bool = False) -> torch.Tensor:
+        n = xyz.shape[0]
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=xyz.device)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        check(lib.kpme_gpu_plan_execute_device(self._h, n, _ptr(xyz), _ptr(q), _ptr(out),
+                                               _lib.DEFER_CHECKS if defer_checks else 0))
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
+        return out
+
+    def execute_host(self, xyz: np.ndarray, q: np.ndarray, out: np.ndarray | None = None):
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        n = xyz.shape[0]
+        if out is None:
+            out = np.zeros(max(n, 1))
+        dp = C.POINTER(C.c_double)
+        check(lib.kpme_gpu_plan_execute(self._h, n, xyz.ctypes.data_as(dp), q.ctypes.data_as(dp),
+                                        out.ctypes.data_as(dp)))
+        return out[:n]
+
+    def execute_host_ptr(self, n: int, xyz_ptr: int, q_ptr: int, out_ptr: int):
+        dp = C.POINTER(C.c_double)
+        check(lib.kpme_gpu_plan_execute(self._h, n, C.cast(xyz_ptr, dp), C.cast(q_ptr, dp),
+                                        C.cast(out_ptr, dp)))
+
+    def status(self):
+        check(lib.kpme_gpu_plan_status(self._h))
+
+    def launches(self) -> int:
+        return lib.kpme_gpu_plan_launches(self._h)
+
+    def close(self):
+        if self._h:
+            lib.kpme_gpu_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def kron_matvec_dense(A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, x: torch.Tensor,

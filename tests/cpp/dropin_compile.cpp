@@ -28,6 +28,13 @@ ref::KpmeResult run(const ref::EwaldConfig& c, const ref::CellGrid& g,
                     const ref::ChargeVector& q) {
     auto a = kpme_b200::kpme_apply(c, g, 4, d, p, q, ref::KpmeOptions{});
     (void)a;
+    // the reference's six-argument call form (KpmeOptions defaulted)
+    auto b = kpme_b200::kpme_apply<ref::KpmeResult>(c, g, 4, d, p, q);
+    (void)b;
+    kpme_b200::GpuOptions multi;
+    multi.devices = {0, 1, 2, 3};
+    auto m = kpme_b200::kpme_apply(c, g, 4, d, p, q, ref::KpmeOptions{}, multi);
+    (void)m;
     kpme_b200::Plan plan(c, g, 4, d, ref::KpmeOptions{}, 16);
     return kpme_b200::kpme_apply<ref::KpmeResult>(c, g, 4, d, p, q, ref::KpmeOptions{});
 }

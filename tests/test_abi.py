@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     missing = [f for f in declared if f not in exported]
     assert not missing, missing
     assert sorted(_lib.EXPORTS) == declared
-    assert _lib.lib.kpme_gpu_abi_version() == 1
+    assert _lib.lib.kpme_gpu_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_library_is_sm100a():

@@ -23,3 +23,25 @@ def test_cpp_dropin_cfg1(tmp_path, golden):
     ref = golden["e2e_cfg1_pot"]
     assert np.linalg.norm(z - ref) / np.linalg.norm(ref) <= 1e-10
     assert out[1001].startswith("invalid_argument assign_particles: particle 7 outside the box")
+
+
+ACC_GPU = os.path.join(ROOT, "oracle", "_ref", "kpme_acceptance_gpu")
+
+
+@pytest.mark.skipif(not os.path.exists(ACC_GPU),
+                    reason="oracle/_ref not built (needs /root/reference at build time)")
+def test_reference_acceptance_gate_on_gpu():
+    """The reference's own acceptance.cpp, unmodified, with kpme::kpme_apply
+    routed to libkpme_b200.so by include/kpme_b200/reroute.hpp (built by
+    oracle/ref/Makefile): its eight criteria -- oracle equivalence,
+    convergence in the order, decomposition invariance across rank grids,
+    the message ledger (acceptance.cpp:50-424) -- pass on the B200."""
+    out = subprocess.run(["nm", "-D", "--undefined-only", ACC_GPU], capture_output=True,
+                         text=True, check=True).stdout
+    assert "kpme_gpu_apply" in out  # the call sites really go through the C ABI
+    env = dict(os.environ, KPME_DATA_DIR=os.path.join(ROOT, "oracle", "_ref", "data"))
+    r = subprocess.run([ACC_GPU], capture_output=True, text=True, timeout=600, env=env)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("PASS criterion") == 8
+    assert "FAIL" not in r.stdout

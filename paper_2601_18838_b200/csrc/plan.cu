@@ -152,6 +152,29 @@ void forward_core(kpme_gpu_plan p, kb::ColumnArgs a, double* core) {
     }
 }
 
+// Backward expansions + gather - c sum(q) from the summed core. The
+// templated gathers (L <= 8 in the monomial basis, L = 10, 12) rebuild their
+// column's B2 block from the core in the prologue; other orders run the core
+// backward kernel to B2 (and c * sum q) first, then the generic gather.
+bool gather_rebuilds_b2(int L) { return L <= 8 || L == 10 || L == 12; }
+
+void backward_gather(kpme_gpu_plan p, kb::ColumnArgs a, const double* core) {
+    a.Fc = core;
+    if (gather_rebuilds_b2(p->g.L)) {
+        a.B2 = nullptr;
+        a.corr = nullptr;
+        if (p->g.L <= 8) mono_tables(p, a);
+    } else {
+        kb::launch_core_backward(p->g, p->G, core, p->correction, p->W[0], p->W[1], p->B2,
+                                 p->corr, p->stream);
+        a.B2 = p->B2;
+        a.corr = p->corr;
+        p->launches += 1;
+    }
+    kb::launch_bwd_gather(a, kb::GATHER_FROM_B2, p->stream);
+    p->launches += 1;
+}
+
 // The steady-state pipeline on device buffers.
 void pipeline(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q, double* out) {
     if (n > p->cap) invalid("kpme_gpu: more particles than the plan was created for");
@@ -191,13 +214,8 @@ void pipeline(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q, do
     }
     record(p, 3);
     // backward x, y, z expansions + gather - c sum(q), B2 rebuilt per column
-    a.B2 = nullptr;
-    a.Fc = p->F;
-    a.corr = nullptr;
-    if (p->g.L <= 8) mono_tables(p, a);
-    kb::launch_bwd_gather(a, kb::GATHER_FROM_B2, p->stream);
+    backward_gather(p, a, p->F);
     record(p, 4);
-    p->launches += 1;
 }
 
 // First half for slab plans: sort .. forward contractions into core.
@@ -217,12 +235,7 @@ void backward_half(kpme_gpu_plan p, const double* core, double* out) {
     kb::ColumnArgs a = column_args(p);
     a.out = out;
     a.gpairs = gather_pairs(p->g, p->last_n);
-    a.B2 = nullptr;
-    a.Fc = core;
-    a.corr = nullptr;
-    if (p->g.L <= 8) mono_tables(p, a);
-    kb::launch_bwd_gather(a, kb::GATHER_FROM_B2, p->stream);
-    p->launches += 1;
+    backward_gather(p, a, core);
 }
 
 // ---- pipelined host path ------------------------------------------------------

@@ -483,6 +483,23 @@ def test_e2e_orders_vs_oracle(oracle, order, modes, counts):
     assert rel(z, oracle.kpme_apply(pb)) <= E2E_TOL
 
 
+@pytest.mark.parametrize("order", [9, 10, 11, 12, 13, 14, 15, 16])
+def test_e2e_high_orders_vs_oracle(oracle, order):
+    """Orders above 8 up to the CLI's maximum 16 (tools/kpme.cpp:343): the
+    generic spread and gather (odd L and L > 12 run the core backward kernel
+    before the gather), both with several cells and with the one-cell grids of
+    acceptance criterion 2 (acceptance.cpp:79-105), against the oracle."""
+    from oracle.binding import make_problem
+
+    for counts, n, modes in (((2, 3, 2), 800, 3), ((1, 1, 1), 32, 2)):
+        pb = make_problem(oracle, n=n, counts=counts, order=order, modes=modes, eps=1e-12,
+                          seed=order, charges="neutral")
+        plan = plan_for(pb)
+        z = plan.execute(dev(pb.pos), dev(pb.q)).cpu().numpy()
+        assert rel(z, oracle.kpme_apply(pb)) <= E2E_TOL
+        assert rel(plan.execute_host(pb.pos, pb.q), z) <= 1e-14
+
+
 @pytest.mark.parametrize("order", [4, 6, 8])
 def test_e2e_clustered_cells(oracle, order):
     """Most particles in a few cells: long chunk streams inside one cell, warps

@@ -45,6 +45,8 @@ def args_():
                    help="use the z-slab path (SlabPlan + NCCL core all-reduce) even on 1 GPU")
     p.add_argument("--rank-grid", default=None,
                    help="P0xP1xP2 device grid of cell blocks for N > 1 (default 1x1xN: z-slabs)")
+    p.add_argument("--cfg5-meshes", default=None, help="cfg5: comma list of n (default 64..512)")
+    p.add_argument("--cfg5-ranks", default=None, help="cfg5: comma list of R (default 4..64)")
     return p.parse_args()
 
 
@@ -231,9 +233,9 @@ def mesh_work(w, ms):
     the term-collapsed form, (W0 (x) W1 (x) W2) then G .* then the transposes,
     2 (2 R n^3 + 2 R^2 n^2 + 2 R^3 n) + R^3 flops with R = 2M+1,
     fused into the spread and gather kernels, so it is quoted per whole step.
-    Beside it, the reference's per-term SPKMV flops 12 |Lambda| r_ax n^3
-    (r_ax = 2(M+1), SURVEY.md §8(d) F form) over the same step time: the
-    throughput the reference's formulation would need to match this step."""
+    The reference's per-term SPKMV flop count 12 |Lambda| r_ax n^3 (r_ax =
+    2(M+1), SURVEY.md §8(d) F form) is listed as a count only: it is work the
+    collapsed form does not do, not a throughput."""
     L, M = w.order, w.cfg.modes
     R, r_ax = 2 * M + 1, 2 * (M + 1)
     n = [k * L for k in w.grid.counts]
@@ -242,37 +244,50 @@ def mesh_work(w, ms):
     spkmv = 12.0 * len(w.dec.terms) * r_ax * n3
     return {"formulation": "collapsed (fused into spread/gather; per whole step)",
             "collapsed_flops": collapsed, "gflops": collapsed / (ms * 1e-3) / 1e9,
-            "reference_spkmv_flops": spkmv,
-            "reference_spkmv_equivalent_gflops": spkmv / (ms * 1e-3) / 1e9}
+            "reference_spkmv_flops_not_executed": spkmv}
 
 
-def spread_algorithmic(w, S):
+def local_shape(w, block=None):
+    """Cells per axis of the plan's block (the whole grid for one plan)."""
+    K = list(w.grid.counts)
+    if block is not None:
+        K = [hi - lo for lo, hi in block]
+    return K
+
+
+def sort_algorithmic(n):
+    """Cell sort + permute (geometry.hpp:131-154): compulsory HBM traffic is
+    the particles read once (x, y, z, q: 32 B) and the cell-ordered records
+    plus the permutation written once (32 + 4 B); the cell offsets are
+    negligible. Counting passes are the implementation's, not algorithmic."""
+    return 0.0, 68.0 * n
+
+
+def spread_algorithmic(w, n, K, S):
     """Algorithmic work of the fused spread + forward-z kernel per launch
     (DESIGN.md §4): flops 2 L^3 N (accumulate) + 2 R L^3 per cell
     (contraction); bytes 32 N (sorted x,y,z,q) + 4 (ncell+1) (offsets) +
-    8 S n0 n1 R (column partials written)."""
+    8 S K0 K1 (R^3 + 1) (per-column partial cores written)."""
     L, R = w.order, 2 * w.cfg.modes + 1
-    K = w.grid.counts
-    n0, n1 = K[0] * L, K[1] * L
     ncell = K[0] * K[1] * K[2]
-    flops = 2.0 * L ** 3 * w.n + 2.0 * R * L ** 3 * ncell
-    bytes_ = 32.0 * w.n + 4.0 * (ncell + 1) + 8.0 * S * n0 * n1 * R
+    flops = 2.0 * L ** 3 * n + 2.0 * R * L ** 3 * ncell
+    bytes_ = 32.0 * n + 4.0 * (ncell + 1) + 8.0 * S * K[0] * K[1] * (R ** 3 + 1)
     return flops, bytes_
 
 
-def gather_algorithmic(w):
+def gather_algorithmic(w, n, K):
     """backward-z + gather kernel: flops 2 L^3 N + 2 R L^3 ncell; bytes 32 N
     (sorted particles) + 4 N (perm) + 8 N (potentials) + 8 n0 n1 R (B2)."""
     L, R = w.order, 2 * w.cfg.modes + 1
-    K = w.grid.counts
     ncell = K[0] * K[1] * K[2]
-    flops = 2.0 * L ** 3 * w.n + 2.0 * R * L ** 3 * ncell
-    bytes_ = 44.0 * w.n + 8.0 * K[0] * L * K[1] * L * R + 4.0 * (ncell + 1)
+    flops = 2.0 * L ** 3 * n + 2.0 * R * L ** 3 * ncell
+    bytes_ = 44.0 * n + 8.0 * K[0] * L * K[1] * L * R + 4.0 * (ncell + 1)
     return flops, bytes_
 
 
 def ncu_traffic(kernel_key):
-    """dram bytes per launch from the committed ncu --set full summary."""
+    """dram bytes per launch from the committed ncu --set full summary
+    (profiles/ncu_summary.json, captured from this bench's workload)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
@@ -282,12 +297,55 @@ def ncu_traffic(kernel_key):
         return None
 
 
+def stage_rooflines(torch, plan, run_eager, w, n, K, flush, steps, peaks, fp64):
+    """Per-stage device times (the plan's own CUDA events on its stream,
+    averaged over eager steps with an L2 flush before each) and each stage's
+    roofline: the sort against HBM, the spread and gather against
+    max(HBM, FP64)."""
+    plan.enable_timing(True)
+    acc, cnt = None, max(3, min(steps, 10))
+    for _ in range(cnt):
+        flush.zero_()
+        run_eager()
+        st = plan.stage_times()
+        acc = st if acc is None else [x + y for x, y in zip(acc, st)]
+    plan.enable_timing(False)
+    st = [x / cnt for x in acc]
+    stages = {"sort_permute_ms": st[0], "spread_fwd_ms": st[1], "core_ms": st[2],
+              "bwd_gather_ms": st[3]}
+    S = max(1, min(K[2], (3 * 148) // max(1, K[0] * K[1])))
+    hbm = peaks["hbm_gbs"]
+    out = {}
+    for name, t_ms, (flops, bytes_) in (("k_sort", st[0], sort_algorithmic(n)),
+                                       ("k_spread_fwd", st[1], spread_algorithmic(w, n, K, S)),
+                                       ("k_bwd_gather", st[3], gather_algorithmic(w, n, K))):
+        t_hbm = bytes_ / (hbm * 1e9)
+        t_fp = flops / (fp64 * 1e12) if flops else 0.0
+        if t_fp >= t_hbm:
+            ach = flops / (t_ms * 1e-3) / 1e12
+            r = {"bound": "fp64", "achieved": ach, "peak": fp64, "unit": "TFLOP/s",
+                 "frac": ach / fp64,
+                 "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (the DMMA tensor "
+                                "subpipe; MEASURED_PEAKS.json has no FP64 entry)",
+                 "hbm_frac": bytes_ / (t_ms * 1e-3) / 1e9 / hbm}
+        else:
+            ach = bytes_ / (t_ms * 1e-3) / 1e9
+            r = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        r.update({"kernel": name, "algorithmic_flops": flops, "algorithmic_bytes": bytes_,
+                  "kernel_ms": t_ms, "traffic": ncu_traffic(name),
+                  "traffic_source": "profiles/ncu_summary.json (ncu --set full of this workload)"})
+        out[name] = r
+    return stages, out
+
+
 def run_ours(a):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    if torch.cuda.device_count() < 1:
+        raise SystemExit("bench.py: no CUDA device")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     slab = world > 1 or a.slab
@@ -296,6 +354,8 @@ def run_ours(a):
     from paper_2601_18838_b200 import inputs
     from paper_2601_18838_b200.plan import KpmePlan
 
+    if a.workload == "cfg5":
+        return run_cfg5(a, torch, dist, rank, world, dev)
     w = inputs.workload(a.workload)
     peaks, peaks_src = load_peaks()
     flush = torch.empty(FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
@@ -304,8 +364,10 @@ def run_ours(a):
         from paper_2601_18838_b200.dist import SlabPlan
 
         dims = tuple(int(v) for v in a.rank_grid.split("x")) if a.rank_grid else None
-        plan = SlabPlan(w, rank, world, device=local, dims=dims)
-        step, e2e_step, launches, meta = plan.bench_callables()
+        sp = SlabPlan(w, rank, world, device=local, dims=dims)
+        step, e2e_step, launches, meta = sp.bench_callables()
+        plan, n_local, K_local = sp.plan, sp.n, local_shape(w, sp.block)
+        xyz, q, out = sp.xyz, sp.q, sp.out
     else:
         plan = KpmePlan(w.cfg, w.grid, w.order, w.dec, w.n, device=local)
         xyz = torch.as_tensor(w.data.cloud.positions, device=dev).contiguous()
@@ -314,6 +376,7 @@ def run_ours(a):
         plan.execute(xyz, q, out)  # validates inputs (synchronous checks)
         plan.execute_graph(xyz, q, out)
         launches = plan.launches()
+        n_local, K_local = w.n, local_shape(w)
 
         def step():
             plan.execute_graph(xyz, q, out)
@@ -326,6 +389,9 @@ def run_ours(a):
             plan.execute_host_ptr(w.n, xyz_h.data_ptr(), q_h.data_ptr(), out_h.data_ptr())
 
         meta = {}
+
+    def run_eager():
+        plan.execute(xyz, q, out, defer_checks=True)
 
     clocks = Clocks(local)
     clocks.start()
@@ -345,8 +411,7 @@ def run_ours(a):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    if not slab:
-        plan.status()  # deferred argument checks of the timed region
+    plan.status()  # deferred argument checks of the timed region
 
     # e2e through the public API with host buffers
     for _ in range(2):
@@ -354,52 +419,20 @@ def run_ours(a):
     e2e_times = timed_steps(torch, e2e_step, a.steps, flush)
     e2e_ms = sum(e2e_times) / len(e2e_times)
     e2e_sorted = sorted(e2e_times)
-    e2e_spread = {"min": e2e_sorted[0], "median": e2e_sorted[len(e2e_sorted) // 2], "max": e2e_sorted[-1]}
+    e2e_spread = {"min": e2e_sorted[0], "median": e2e_sorted[len(e2e_sorted) // 2],
+                  "max": e2e_sorted[-1]}
     if dist.is_initialized():
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
-    # per-stage times (eager, timing events) -> dominant kernel roofline
-    roofline, stages = None, None
-    if not slab:
-        plan.enable_timing(True)
-        acc = None
-        for _ in range(max(3, min(a.steps, 10))):
-            flush.zero_()
-            plan.execute(xyz, q, out, defer_checks=True)
-            st = plan.stage_times()
-            acc = st if acc is None else [x + y for x, y in zip(acc, st)]
-        cnt = max(3, min(a.steps, 10))
-        plan.enable_timing(False)
-        st = [x / cnt for x in acc]
-        stages = {"sort_permute_ms": st[0], "spread_fwd_ms": st[1], "core_ms": st[2],
-                  "bwd_gather_ms": st[3]}
-        S = max(1, min(w.grid.counts[2], (3 * 148) // (w.grid.counts[0] * w.grid.counts[1])))
-        fp64 = fp64_peak(torch, dev)
-        cand = {"k_spread_fwd": (st[1], spread_algorithmic(w, S)),
-                "k_bwd_gather": (st[3], gather_algorithmic(w))}
-        name = max(cand, key=lambda k: cand[k][0])
-        t_ms, (flops, bytes_) = cand[name]
-        t_hbm = bytes_ / (peaks["hbm_gbs"] * 1e9)
-        t_fp64 = flops / (fp64 * 1e12)
-        if t_fp64 >= t_hbm:
-            achieved = flops / (t_ms * 1e-3) / 1e12
-            roofline = {"bound": "fp64", "kernel": name, "achieved": achieved, "peak": fp64,
-                        "unit": "TFLOP/s", "frac": achieved / fp64,
-                        "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (the DMMA "
-                                       "tensor subpipe, 64 FP64 FMA/clk/SM; the spread's "
-                                       "GEMM-shaped work runs there)",
-                        "hbm_frac": bytes_ / (t_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}
-        else:
-            achieved = bytes_ / (t_ms * 1e-3) / 1e9
-            roofline = {"bound": "hbm", "kernel": name, "achieved": achieved,
-                        "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                        "frac": achieved / peaks["hbm_gbs"],
-                        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks_src})"}
-        roofline.update({"algorithmic_flops": flops, "algorithmic_bytes": bytes_,
-                         "kernel_ms": t_ms, "traffic": ncu_traffic(name)})
-        meta["fp64_dgemm_tflops"] = fp64
+    # per-stage times (eager, the plan's timing events) -> rooflines
+    fp64 = fp64_peak(torch, dev)
+    stages, rooflines = stage_rooflines(torch, plan, run_eager, w, n_local, K_local, flush,
+                                        a.steps, peaks, fp64)
+    dom = max(("k_spread_fwd", "k_bwd_gather", "k_sort"), key=lambda k: rooflines[k]["kernel_ms"])
+    roofline = rooflines[dom]
+    meta["fp64_dgemm_tflops"] = fp64
 
     if rank != 0:
         if dist.is_initialized():
@@ -408,7 +441,6 @@ def run_ours(a):
         return
 
     value = w.n / (ms * 1e-3)
-    mesh = mesh_work(w, ms)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -416,20 +448,22 @@ def run_ours(a):
         "data": "synthetic (seeded splitmix64 sample_cloud, BASELINE.json config shapes)",
         "config": w.describe(),
         "impl_config": {"formulation": "collapsed (term-collapsed SKP core, per-shape chooser)",
-                        "parallelism": (f"rank grid {'x'.join(map(str, plan.dims))} of cell "
-                                        f"blocks (NCCL core all-reduce)") if slab else "1 GPU",
-                        "l2": "flushed (256 MiB write) before every timed step"},
+                        "parallelism": (f"rank grid {'x'.join(map(str, sp.dims))} of cell "
+                                        f"blocks, one process per GPU, plan-owned NCCL core "
+                                        f"all-reduce") if slab else "1 GPU",
+                        "l2": "flushed (256 MiB write) before every timed step",
+                        "timing": "CUDA events per step, max over ranks"},
         "e2e": {"value": w.n / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "ms_per_step_spread": e2e_spread,
                 "h2d_bytes_per_step": 32 * w.n, "d2h_bytes_per_step": 8 * w.n,
-                "path": ("SlabPlan.e2e_step: pinned H2D of the slab's particles, forward, "
-                         "NCCL core all-reduce, backward, D2H" if slab else
-                         "KpmePlan.execute_host_ptr -> kpme_gpu_plan_execute (pinned host "
-                         "xyz/q in, potentials out)")},
-        "mesh": mesh,
+                "path": "kpme_gpu_plan_execute (pinned host xyz/q in, potentials out)" +
+                        ("; per rank: its cell block's particles, NCCL core all-reduce inside"
+                         if slab else "")},
+        "mesh": mesh_work(w, ms),
         "gpu_launches": launches * a.steps,
         "clocks": clk,
         "roofline": roofline,
+        "rooflines": rooflines,
         "stages": stages,
         **meta,
     }
@@ -445,13 +479,36 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+def oneshot_e2e(w, reps=5):
+    """kpme_apply through the one-shot drop-in (kpme_gpu_apply: cached plan,
+    pageable numpy buffers, H2D / D2H inside): host wall clock around the
+    synchronous call, first (cold: plan build) and steady-state."""
+    import paper_2601_18838_b200 as kp
+
+    kp._lib.lib.kpme_gpu_apply_cache_clear()
+    t0 = time.perf_counter()
+    kp.kpme_apply(w.cfg, w.grid, w.order, w.dec, w.data.cloud, w.data.charges)
+    cold = time.perf_counter() - t0
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        kp.kpme_apply(w.cfg, w.grid, w.order, w.dec, w.data.cloud, w.data.charges)
+        ts.append(time.perf_counter() - t0)
+    kp._lib.lib.kpme_gpu_apply_cache_clear()
+    med = statistics.median(ts)
+    return {"value": w.n / med, "unit": UNIT, "ms_per_call": med * 1e3,
+            "first_call_ms": cold * 1e3,
+            "path": "kpme_apply -> kpme_gpu_apply (plan cache), pageable numpy in/out, host "
+                    "wall clock around the synchronous call"}
+
+
 def extras(torch, dev, flush, steps):
-    """Other BASELINE configs on one GPU (same timing rules), and one config-5
-    dense-operator point on DMMA."""
+    """Other BASELINE configs on one GPU (same timing rules), the one-shot
+    drop-in latency, and one config-5 dense-operator point on DMMA."""
     from paper_2601_18838_b200 import inputs
     from paper_2601_18838_b200.plan import KpmePlan, dense_workspace_bytes, kron_matvec_dense
 
-    out = {}
+    out = {"e2e_oneshot_cfg3": oneshot_e2e(inputs.workload("cfg3"))}
     for name in ("cfg1", "cfg2", "cfg4"):
         w = inputs.workload(name)
         plan = KpmePlan(w.cfg, w.grid, w.order, w.dec, w.n, device=dev.index)
@@ -479,6 +536,78 @@ def extras(torch, dev, flush, steps):
     out["cfg5_dense_256_R16"] = {"mesh_gflops": flops / (ms * 1e-3) / 1e9, "ms": ms,
                                  "flops_formula": "6 R n^4 (op_count_estimate x2, kron.hpp:201-211)"}
     return out
+
+
+def run_cfg5(a, torch, dist, rank, world, dev):
+    """Config 5: the dense SKP grid operator on z-slabs, every mesh and rank
+    of BASELINE (64^3..512^3, R in {4..64}), all three sharded-axis strategies
+    timed per shape (max over ranks, CUDA events, L2 flushed) and the faster
+    one chosen -- the north star's slab all-to-all vs rank-split + reduce,
+    plus the reference's own SPKMV-style reduction (parallel.hpp:169-176).
+    Prints the strategy table on stderr and one JSON line."""
+    from paper_2601_18838_b200 import inputs
+    from paper_2601_18838_b200.dist import DenseSlabOperator, slab_bounds
+    from paper_2601_18838_b200.plan import KpmePlan, dgemm_tn
+
+    meshes = [int(v) for v in (a.cfg5_meshes or "64,128,256,512").split(",")]
+    ranks = [int(v) for v in (a.cfg5_ranks or "4,8,16,32,64").split(",")]
+    flush = torch.empty(FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
+    peaks, _ = load_peaks()
+    fp64 = fp64_peak(torch, dev)
+    rows = []
+    for n in meshes:
+        cfg, grid, L, dec = inputs.dense_case(n, max(ranks))
+        plan = KpmePlan(cfg, grid, L, dec, 1, device=dev.index)
+        ops_all = [plan.axis_operands(ax) for ax in range(3)]
+        plan.close()
+        lo, hi = slab_bounds(n, rank, world)
+        g = torch.Generator(device=dev).manual_seed(n)
+        x_full = torch.randn(n, n, n, dtype=torch.float64, device=dev, generator=g)
+        x_local = x_full[:, :, lo:hi].contiguous()
+        del x_full
+        for R in ranks:
+            ops = [o[:R].contiguous() for o in ops_all]
+            op = DenseSlabOperator(*ops, (n, n, n), lambda i, f, o, acc: dgemm_tn(i, f, o, acc))
+            tms = {}
+            for s in DenseSlabOperator.STRATEGIES:
+                op.apply(x_local, s)
+                torch.cuda.synchronize()
+                if dist.is_initialized():
+                    dist.barrier()
+                reps = 3 if n <= 256 else 1
+                t = timed_steps(torch, lambda: op.apply(x_local, s), reps, flush)
+                ms = sum(t) / len(t)
+                if dist.is_initialized():
+                    tt = torch.tensor([ms], device=dev)
+                    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                    ms = float(tt.item())
+                tms[s] = ms
+            best = min(tms, key=tms.get)
+            flops = 6.0 * R * n ** 4
+            rows.append({"n": n, "R": R, "ms": tms, "chosen": best,
+                         "mesh_gflops": flops / (tms[best] * 1e-3) / 1e9,
+                         "frac_of_fp64": flops / (tms[best] * 1e-3) / 1e12 / fp64})
+            if rank == 0:
+                sys.stderr.write(f"cfg5 n={n:4d} R={R:3d} " + " ".join(
+                    f"{k}={v:9.3f}ms" for k, v in tms.items()) + f"  -> {best}\n")
+            del op, ops
+        del ops_all, x_local
+        torch.cuda.empty_cache()
+    if rank == 0:
+        head = max(rows, key=lambda r: (r["n"], r["R"]))
+        line = {"metric": "SKP grid operator mesh GFLOP/s (FP64, dense factors)",
+                "value": head["mesh_gflops"], "unit": "GFLOP/s", "n_gpus": world,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": head["ms"][head["chosen"]],
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (N(0,1) mesh, factors from the SKP "
+                                         "construction, BASELINE config 5)",
+                "config": {"workload": "cfg5", "mesh": [head["n"]] * 3, "skp_terms": head["R"]},
+                "strategies": rows, "fp64_dgemm_tflops": fp64,
+                "flops_formula": "6 R n^4 (op_count_estimate x2, kron.hpp:201-211)"}
+        emit(line)
+    if dist.is_initialized():
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def run_reference(a):
@@ -521,12 +650,48 @@ def emit(line: dict):
     out.flush()
 
 
+def launch_ranks(a):
+    """``--gpus N`` without a launcher: re-exec this command under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous). Under a
+    launcher the world size must equal N; a mismatch or too few GPUs fails
+    loudly instead of measuring another N."""
+    if "RANK" in os.environ:
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        if world != a.gpus:
+            sys.stderr.write(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}\n")
+            raise SystemExit(2)
+        return
+    if a.gpus <= 1 or a.impl == "reference":
+        return
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        sys.stderr.write(f"bench.py: --gpus {a.gpus} needs {a.gpus} GPUs, this box has {have}\n")
+        raise SystemExit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     global _JSON_OUT
+    a = args_()
+    if a.gpus < 1:
+        sys.stderr.write("bench.py: --gpus must be >= 1\n")
+        raise SystemExit(2)
+    launch_ranks(a)
     sys.stdout.flush()
     _JSON_OUT = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
-    a = args_()
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -152,6 +152,17 @@ void forward_core(kpme_gpu_plan p, kb::ColumnArgs a, double* core) {
     }
 }
 
+// One rank of a multi-process job (a plan with an attached communicator):
+// sum the partial cores of all ranks -- the collapsed form's only exchange --
+// before the backward half.
+void allreduce_core(kpme_gpu_plan p, double* core) {
+    if (!p->comm) return;
+    const ncclResult_t r = ncclAllReduce(core, core, (size_t)p->g.R * p->g.R * p->g.R + 1,
+                                         ncclDouble, ncclSum, p->comm, p->stream);
+    if (r != ncclSuccess)
+        throw Error(KPME_GPU_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+}
+
 // Backward expansions + gather - c sum(q) from the summed core. The
 // templated gathers (L <= 8 in the monomial basis, L = 10, 12) rebuild their
 // column's B2 block from the core in the prologue; other orders run the core
@@ -204,14 +215,7 @@ void pipeline(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q, do
     }
     // spread + z, y, x forward contractions -> one partial core per column
     forward_core(p, a, p->F);
-    if (p->comm) {
-        // one rank of a multi-process job: sum the partial cores of all ranks
-        // (the collapsed form's only exchange) before the backward half
-        const ncclResult_t r = ncclAllReduce(p->F, p->F, (size_t)p->g.R * p->g.R * p->g.R + 1,
-                                             ncclDouble, ncclSum, p->comm, p->stream);
-        if (r != ncclSuccess)
-            throw Error(KPME_GPU_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
-    }
+    allreduce_core(p, p->F);
     record(p, 3);
     // backward x, y, z expansions + gather - c sum(q), B2 rebuilt per column
     backward_gather(p, a, p->F);
@@ -392,6 +396,7 @@ void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double
     }
     kb::launch_core_sum(g, C * nb, p->cFpart, p->F, p->stream);
     ++p->launches;
+    allreduce_core(p, p->F);
     tr.mark("core sum", p->stream);
     // backward + gather per chunk; its potentials leave while the next runs
     for (int i = 0; i < C; ++i) {

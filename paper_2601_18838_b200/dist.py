@@ -130,10 +130,16 @@ class SlabPlan:
     slab (or, with ``dims = (P0, P1, P2)``, to its cell block of a general
     device grid, ranks flattened like RankGrid, parallel.hpp:46-82), builds
     the plan and exposes the timed callables. The exchange is the same single
-    core all-reduce for every grid shape."""
+    core all-reduce for every grid shape.
+
+    Under an initialised process group the plan owns its NCCL communicator
+    (``KpmePlan.attach_comm``; the 128-byte id is broadcast once through the
+    group): the library runs forward half -> ncclAllReduce -> backward half
+    on its own stream, captured as one CUDA graph, and the host path
+    (``kpme_gpu_plan_execute``) includes the same exchange."""
 
     def __init__(self, w, rank: int, world: int, device: int = 0, group=None, dims=None):
-        from .plan import KpmePlan
+        from .plan import KpmePlan, nccl_unique_id
 
         self.w, self.rank, self.world = w, rank, world
         self.dims = tuple(dims) if dims is not None else (1, 1, world)
@@ -149,50 +155,45 @@ class SlabPlan:
         dev = torch.device("cuda", device)
         self.plan = KpmePlan(w.cfg, w.grid, w.order, w.dec, max(1, len(self.idx)), device=device,
                              block=self.block)
+        if dist.is_initialized():
+            uid = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0, group=group)
+            self.plan.attach_comm(world, rank, uid[0])
+        self.library_comm = dist.is_initialized()
         self.driver = SlabDriver(self.plan, group, dev)
         pos = w.data.cloud.positions[self.idx]
         q = w.data.charges.values[self.idx]
+        self.n = len(self.idx)
         self.xyz = torch.as_tensor(pos, device=dev).contiguous()
         self.q = torch.as_tensor(q, device=dev).contiguous()
-        self.out = torch.empty(len(self.idx), dtype=torch.float64, device=dev)
+        self.out = torch.empty(self.n, dtype=torch.float64, device=dev)
         self.xyz_h = torch.as_tensor(pos).contiguous().pin_memory()
         self.q_h = torch.as_tensor(q).contiguous().pin_memory()
-        self.out_h = torch.empty(len(self.idx), dtype=torch.float64).pin_memory()
-        self.driver.apply(self.xyz, self.q, self.out)
+        self.out_h = torch.empty(self.n, dtype=torch.float64).pin_memory()
+        self.apply()
         self.plan.status()
-        self.graph = None
-        self.graph_error = None
 
-    def capture(self) -> bool:
-        """Capture the whole slab step (forward kernels, NCCL core all-reduce,
-        backward kernels) into one CUDA graph; stays eager if capture fails."""
-        try:
-            side = torch.cuda.Stream()
-            side.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(side):
-                for _ in range(2):
-                    self.driver.apply(self.xyz, self.q, self.out)
-            torch.cuda.current_stream().wait_stream(side)
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self.driver.apply(self.xyz, self.q, self.out)
-            g.replay()
-            torch.cuda.synchronize()
-            self.graph = g
-        except Exception as e:  # pragma: no cover - depends on the NCCL build
-            self.graph, self.graph_error = None, repr(e)
-            torch.cuda.synchronize()
-        return self.graph is not None
+    def apply(self):
+        if self.library_comm:
+            self.plan.execute(self.xyz, self.q, self.out, defer_checks=True)
+        else:
+            self.driver.apply(self.xyz, self.q, self.out)
 
     def step(self):
-        if self.graph is not None:
-            self.graph.replay()
+        """One device-resident step: the plan's captured graph (sort, spread,
+        contractions, NCCL core all-reduce, gather)."""
+        if self.library_comm:
+            self.plan.execute_graph(self.xyz, self.q, self.out)
         else:
             self.driver.apply(self.xyz, self.q, self.out)
 
     def e2e_step(self):
-        """Host in, host out: H2D of the local particles, the step, D2H."""
+        """Host in, host out through kpme_gpu_plan_execute (pinned buffers):
+        H2D of the local particles, the pipeline with its exchange, D2H."""
+        if self.library_comm:
+            self.plan.execute_host_ptr(self.n, self.xyz_h.data_ptr(), self.q_h.data_ptr(),
+                                       self.out_h.data_ptr())
+            return
         self.xyz.copy_(self.xyz_h, non_blocking=True)
         self.q.copy_(self.q_h, non_blocking=True)
         self.driver.apply(self.xyz, self.q, self.out)
@@ -201,13 +202,11 @@ class SlabPlan:
 
     def bench_callables(self):
         launches = self.plan.launches()
-        self.capture()
         meta = {"rank_grid": list(self.dims), "cell_block": [list(b) for b in self.block],
-                "local_particles": int(len(self.idx)),
-                "exchange": f"all_reduce of {self.plan.core_size()} doubles per step",
-                "cuda_graph": self.graph is not None}
-        if self.graph_error:
-            meta["cuda_graph_error"] = self.graph_error[:200]
+                "local_particles": int(self.n),
+                "exchange": (f"ncclAllReduce of {self.plan.core_size()} doubles per step on the "
+                             f"plan's own communicator" if self.library_comm else "none (1 rank)"),
+                "cuda_graph": True}
         return self.step, self.e2e_step, launches, meta
 
     def gather_global(self) -> np.ndarray:

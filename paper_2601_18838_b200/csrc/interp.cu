@@ -976,6 +976,269 @@ __global__ void __launch_bounds__(32 * UV_NW, SPREAD_MINB) k_spread_uv(ColumnArg
     spread_epilogue<L, NW>(a, cr, sm, per_warp, M::area, RP, epi, red, qsum, want_fwd);
 }
 
+// ---------------------------------------------------------------------------
+// Spread, split-exponent variant (monomial basis, L = 4 and 6). With m = L/2
+// and every exponent split as e = m e_hi + e_lo (e_hi in {0,1}, e_lo < m),
+//     t0^i t1^j t2^k = [t0^(m ih) t1^(m jh) t2^(m kh)] * [t0^il t1^jl t2^kl],
+// so the cell's L^3 grid is ONE (8 x m^3) = (8 x P)(P x m^3) GEMM:
+//     row g = (ih, jh, kh)  A[g][p]   = q_p T0^ih T1^jh T2^kh  (T = t^m)
+//     col   = (il, jl, kl)  B[p][col] = t0^il t1^jl t2^kl
+// No padded rows (the (L x L^2) form wastes 2 of 8 rows at L = 6) and 27 of
+// 32 columns used at L = 6 (all 8 at L = 4): 4 DMMAs per k-step instead of 5.
+// One particle per lane stages its row (no divergent half-warp paths); at
+// L = 6 the B fragment of lane group g at n-tile t < 3 is U_g t0^t with
+// U_g = t1^jl t2^kl over (jl, kl) = (g / 3, g % 3), and tile 3 holds the
+// three (il, 2, 2) columns as W[g] = t0^g t1^2 t2^2.
+template <int L>
+struct F8Map {
+    static_assert(L == 4 || L == 6, "split-exponent spread: L = 4 or 6");
+    static constexpr int m = L / 2;
+    static constexpr int NT = L == 6 ? 4 : 1;
+    static constexpr int SR = 20;              // staged row stride (conflict-free LDS.128)
+    static constexpr int L2 = L * L;
+    static constexpr int MT2 = (L2 + 7) / 8;
+    static constexpr int KS2 = (L + 3) / 4;
+    static constexpr int LDK = KS2 * 4 + 4;
+    static constexpr int stage = 32 * SR;
+    static constexpr int ph = MT2 * 8 * LDK;
+    static constexpr int area = stage + ph;
+    // grid node (i, j, k) of accumulator column `col` at row group g
+    __device__ static int node(int g, int col) {
+        const int ih = (g >> 2) & 1, jh = (g >> 1) & 1, kh = g & 1;
+        int il, jl, kl;
+        if (L == 6) {
+            const int t = col >> 3, c = col & 7;
+            if (t < 3) {
+                il = t;
+                jl = c / 3;
+                kl = c % 3;
+            } else {
+                if (c >= 3) return -1;
+                il = c;
+                jl = kl = 2;
+            }
+        } else {
+            il = (col >> 2) & 1;
+            jl = (col >> 1) & 1;
+            kl = col & 1;
+        }
+        const int i = m * ih + il, j = m * jh + jl, k = m * kh + kl;
+        return (i * L + j) * L + k;
+    }
+};
+
+template <int L>
+__host__ __device__ constexpr int spread_f8_warp_doubles(int R) {
+    return F8Map<L>::area + F8Map<L>::MT2 * 8 * uv_t1_stride(R);
+}
+template <int L>
+__host__ __device__ constexpr size_t spread_f8_smem_doubles(int R, int /*n2*/) {
+    return 4 * (size_t)spread_f8_warp_doubles<L>(R) + (size_t)spread_epilogue_doubles(L, R);
+}
+
+template <int L, int RTM>
+__global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_f8(ColumnArgs a, int want_fwd) {
+    using M = F8Map<L>;
+    constexpr int L3 = L * L * L, NT = M::NT, MT2 = M::MT2, KS2 = M::KS2, LDK = M::LDK, SR = M::SR;
+    constexpr int NW = 4, NTH = 128;
+    const Geometry& g = a.g;
+    const int R = g.R, RT = (R + 7) / 8, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int RP = uv_t1_stride(R), n2 = g.n[2];
+    const ColumnRange cr = column_range(g, a.S);
+    extern __shared__ double sm[];
+    const int per_warp = spread_f8_warp_doubles<L>(R);
+    double* St = sm + warp * per_warp;  // [32][SR] staged particle rows
+    double* ph = St + M::stage;         // [MT2*8][LDK] finished cell grid
+    double* t1w = St + M::area;         // [MT2*8][RP]  warp partial of T1
+    double* epi = sm + NW * per_warp;   // epilogue scratch
+    __shared__ double red[NTH];
+    __shared__ int cst[66];
+    for (int e = lane; e < MT2 * 8 * RP; e += 32) t1w[e] = 0.0;
+    for (int e = lane; e < M::ph; e += 32) ph[e] = 0.0;  // padding stays zero
+    const int col_cell0 = (cr.c0 * g.K[1] + cr.c1) * g.K[2];
+    const int nz = cr.ze - cr.zb;
+    const bool cst_ok = nz + 1 <= 66;
+    if (cst_ok)
+        for (int e = threadIdx.x; e <= nz; e += NTH) cst[e] = a.start[col_cell0 + cr.zb + e];
+    const CellAxis ax0 = cell_axis_tab(a.cellax[0], cr.c0), ax1 = cell_axis_tab(a.cellax[1], cr.c1);
+    const int gg = lane >> 2, tg = lane & 3;
+    double tmax = 0.0, qsum = 0.0;
+    double t1acc[MT2][RTM][2];
+#pragma unroll
+    for (int mt = 0; mt < MT2; ++mt)
+#pragma unroll
+        for (int t = 0; t < RTM; ++t) t1acc[mt][t][0] = t1acc[mt][t][1] = 0.0;
+    __syncthreads();
+    auto cstart = [&](int c2) { return cst_ok ? cst[c2 - cr.zb] : a.start[col_cell0 + c2]; };
+
+    // Warp w takes particles [pw0, pw1), an exact quarter of the column segment
+    // (cells shared by two warps add linearly); whole cells for phi_cells.
+    int zw0, zw1, pw0, pw1;
+    {
+        const int P0 = cstart(cr.zb), P1 = cstart(cr.ze);
+        const int t0 = P0 + (int)((long long)(P1 - P0) * warp / NW);
+        const int t1 = P0 + (int)((long long)(P1 - P0) * (warp + 1) / NW);
+        auto lb = [&](int target) {
+            return warp_lower_bound(a.start, col_cell0 + cr.zb, col_cell0 + cr.ze, target, lane) - col_cell0;
+        };
+        if (a.phi_cells) {
+            zw0 = warp == 0 ? cr.zb : lb(t0);
+            zw1 = warp == NW - 1 ? cr.ze : lb(t1);
+            pw0 = cstart(zw0);
+            pw1 = cstart(zw1);
+        } else {
+            pw0 = t0;
+            pw1 = t1;
+            zw0 = t0 < t1 ? lb(t0 + 1) - 1 : cr.zb;
+            zw1 = t0 < t1 ? lb(t1) : cr.zb;
+        }
+    }
+    // The next chunk's record is loaded one chunk ahead across cell
+    // boundaries (the warp's chunk sequence is cell-aligned), and the one
+    // after that is prefetched into L2.
+    auto cell_lo_p = [&](int c) { return max(cstart(c), pw0); };
+    auto cell_hi_p = [&](int c) { return min(cstart(c + 1), pw1); };
+    int nc2 = zw0, nbase = zw0 < zw1 ? cell_lo_p(zw0) : 0;
+    auto norm = [&](int& c, int& b) {
+        while (c < zw1 && b >= cell_hi_p(c)) {
+            ++c;
+            if (c < zw1) b = cell_lo_p(c);
+        }
+    };
+    norm(nc2, nbase);
+    auto load_at = [&](int c, int b) {
+        return c < zw1 ? ld_rec(a.sp + min(b + lane, cell_hi_p(c) - 1)) : make_double4(0, 0, 0, 0);
+    };
+    double4 nxt = load_at(nc2, nbase);
+    for (int c2 = zw0; c2 < zw1; ++c2) {
+        const int s0 = cell_lo_p(c2), s1 = cell_hi_p(c2);
+        if (s0 >= s1) {
+            if (a.phi_cells)
+                for (int node = lane; node < L3; node += 32)
+                    a.phi_cells[(int64_t)(col_cell0 + c2) * L3 + node] = 0.0;
+            continue;
+        }
+        const CellAxis ax2 = cell_axis_tab(a.cellax[2], c2);
+        double acc[NT][2];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+        for (int base = s0; base < s1; base += 32) {
+            const int cnt = min(32, s1 - base);
+            const double4 pt = nxt;
+            nbase += 32;
+            norm(nc2, nbase);
+            nxt = load_at(nc2, nbase);
+            if (nc2 < zw1 && nbase + 32 < pw1)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(a.sp + min(nbase + 32 + lane, pw1 - 1)));
+            const double q = lane < cnt ? pt.w : 0.0;
+            qsum += q;
+            const double t0 = (pt.x - ax0.mid) * ax0.inv;
+            const double t1 = (pt.y - ax1.mid) * ax1.inv;
+            const double t2 = (pt.z - ax2.mid) * ax2.inv;
+            tmax = fmax(tmax, fmax(fabs(t0), fmax(fabs(t1), fabs(t2))));
+            __syncwarp();  // previous chunk's fragment reads done
+            double* row = St + lane * SR;
+            if (L == 6) {
+                const double a2 = t0 * t0, b2 = t1 * t1, c2v = t2 * t2;
+                const double T0 = a2 * t0, T1 = b2 * t1, T2 = c2v * t2;
+                const double qT1 = q * T1, qT0 = q * T0, qT0T1 = qT0 * T1;
+                const double b1c1 = t1 * t2, b1c2 = t1 * c2v, b2c1 = b2 * t2, b2c2 = b2 * c2v;
+                // [A_g, U_g] pairs, g = (ih, jh, kh) for A and 3 jl + kl for U
+                *reinterpret_cast<double2*>(row + 0) = make_double2(q, 1.0);
+                *reinterpret_cast<double2*>(row + 2) = make_double2(q * T2, t2);
+                *reinterpret_cast<double2*>(row + 4) = make_double2(qT1, c2v);
+                *reinterpret_cast<double2*>(row + 6) = make_double2(qT1 * T2, t1);
+                *reinterpret_cast<double2*>(row + 8) = make_double2(qT0, b1c1);
+                *reinterpret_cast<double2*>(row + 10) = make_double2(qT0 * T2, b1c2);
+                *reinterpret_cast<double2*>(row + 12) = make_double2(qT0T1, b2);
+                *reinterpret_cast<double2*>(row + 14) = make_double2(qT0T1 * T2, b2c1);
+                // [t0, W0, W1, W2] with W_g = t0^g t1^2 t2^2
+                *reinterpret_cast<double2*>(row + 16) = make_double2(t0, b2c2);
+                *reinterpret_cast<double2*>(row + 18) = make_double2(b2c2 * t0, b2c2 * a2);
+            } else {
+                // L = 4: [A_g, B_g], A_g = q t0^(2ih) t1^(2jh) t2^(2kh), B_g = t0^il t1^jl t2^kl
+                const double a2 = t0 * t0, b2 = t1 * t1, c2v = t2 * t2;
+                const double qb = q * b2, qa = q * a2, qab = qa * b2;
+                const double b1c1 = t1 * t2;
+                *reinterpret_cast<double2*>(row + 0) = make_double2(q, 1.0);
+                *reinterpret_cast<double2*>(row + 2) = make_double2(q * c2v, t2);
+                *reinterpret_cast<double2*>(row + 4) = make_double2(qb, t1);
+                *reinterpret_cast<double2*>(row + 6) = make_double2(qb * c2v, b1c1);
+                *reinterpret_cast<double2*>(row + 8) = make_double2(qa, t0);
+                *reinterpret_cast<double2*>(row + 10) = make_double2(qa * c2v, t0 * t2);
+                *reinterpret_cast<double2*>(row + 12) = make_double2(qab, t0 * t1);
+                *reinterpret_cast<double2*>(row + 14) = make_double2(qab * c2v, t0 * b1c1);
+            }
+            __syncwarp();
+            const int ks = (cnt + 3) >> 2;
+            for (int kk = 0; kk < ks; ++kk) {
+                const double* r = St + (kk * 4 + tg) * SR;
+                const double2 au = *reinterpret_cast<const double2*>(r + 2 * gg);
+                if (L == 6) {
+                    const double tt = r[16];
+                    const double w = gg < 3 ? r[17 + gg] : 0.0;
+                    const double b1 = au.y * tt;
+                    dmma884(acc[0], au.x, au.y);
+                    dmma884(acc[3], au.x, w);
+                    dmma884(acc[1], au.x, b1);
+                    dmma884(acc[2], au.x, b1 * tt);
+                } else {
+                    dmma884(acc[0], au.x, au.y);
+                }
+            }
+        }
+        __syncwarp();
+        // accumulator (g, 8t + 2c + e) -> ph[(i, j)][k]
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int nd = M::node(gg, 8 * t + 2 * tg + e);
+                if (nd >= 0) ph[(nd / L) * LDK + nd % L] = acc[t][e];
+            }
+        __syncwarp();
+        if (a.phi_cells)
+            for (int node = lane; node < L3; node += 32)
+                a.phi_cells[(int64_t)(col_cell0 + c2) * L3 + node] = ph[(node / L) * LDK + node % L];
+        if (want_fwd) {
+            // T1c = ph[(i,j)][k] (MT2*8 x LDK) . W2s[k][r] (LDK x RP)
+            double bf[KS2][4];
+            const double* w2c = a.W2 + c2 * L;  // the cell's W2 slice (L1/L2 resident)
+#pragma unroll
+            for (int s = 0; s < KS2; ++s)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int k = s * 4 + (lane & 3), rr = t * 8 + (lane >> 2);
+                    bf[s][t] = (t < RT && k < L && rr < R) ? __ldg(w2c + (int64_t)rr * n2 + k) : 0.0;
+                }
+#pragma unroll
+            for (int mt = 0; mt < MT2; ++mt)
+#pragma unroll
+                for (int s = 0; s < KS2; ++s) {
+                    const double af = ph[(mt * 8 + (lane >> 2)) * LDK + s * 4 + (lane & 3)];
+#pragma unroll
+                    for (int t = 0; t < RTM; ++t)
+                        if (t < RT) dmma884(t1acc[mt][t], af, bf[s][t]);
+                }
+        }
+        __syncwarp();
+    }
+    if (want_fwd) {
+#pragma unroll
+        for (int mt = 0; mt < MT2; ++mt)
+#pragma unroll
+            for (int t = 0; t < RTM; ++t)
+                if (t < RT)
+                    *reinterpret_cast<double2*>(t1w + (mt * 8 + (lane >> 2)) * RP + t * 8 + 2 * (lane & 3)) =
+                        make_double2(t1acc[mt][t][0], t1acc[mt][t][1]);
+        __syncwarp();
+    }
+    // tensor_weights' out-of-cell check, |t| <= 1 + 2e-12 (slack 1e-12 of the width)
+    const unsigned badw = __ballot_sync(0xffffffffu, !(tmax <= 1.0 + 2e-12));
+    if (lane == 0 && badw) atomicOr(&a.bad[1], 1ull);
+    spread_epilogue<L, NW>(a, cr, sm, per_warp, M::area, RP, epi, red, qsum, want_fwd);
+}
+
 // Backward z-expansion + gather with compile-time L: psi for a batch of the
 // column's cells in shared memory, then one thread per particle,
 // z = sum_i w0[i] sum_j w1[j] sum_k w2[k] psi[i][j][k] - c_Lambda sum(q),
@@ -1412,8 +1675,36 @@ void launch_spread_mma_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
 #ifndef SPREAD_UV
 #define SPREAD_UV 1
 #endif
+#ifndef SPREAD_F8
+#define SPREAD_F8 1  // split-exponent spread for L = 4, 6
+#endif
+template <int L>
+bool launch_spread_f8_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
+    if constexpr (L == 4 || L == 6) {
+        const size_t smem = sizeof(double) * spread_f8_smem_doubles<L>(a.g.R, a.g.n[2]);
+        if (!SPREAD_F8 || smem > 200 * 1024 || a.g.R > 32) return false;
+        static PerDevice attr_once;
+        once_per_device(attr_once, [&] {
+            KB_CUDA(cudaFuncSetAttribute(k_spread_f8<L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         200 * 1024));
+            KB_CUDA(cudaFuncSetAttribute(k_spread_f8<L, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         200 * 1024));
+        });
+        const int grid = block_columns(a.g) * a.S;
+        if (a.g.R <= 16)
+            k_spread_f8<L, 2><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+        else
+            k_spread_f8<L, 4><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+        KB_CHECK_LAUNCH();
+        return true;
+    } else {
+        return false;
+    }
+}
+
 template <int L>
 void launch_spread_uv_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
+    if (launch_spread_f8_t<L>(a, want_fwd, s)) return;
     const size_t smem = sizeof(double) * spread_uv_smem_doubles<L>(a.g.R, a.g.n[2]);
     static PerDevice attr_once;
     once_per_device(attr_once, [&] {

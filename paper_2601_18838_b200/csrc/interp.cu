@@ -989,6 +989,19 @@ __global__ void __launch_bounds__(32 * UV_NW, SPREAD_MINB) k_spread_uv(ColumnArg
 // L = 6 the B fragment of lane group g at n-tile t < 3 is U_g t0^t with
 // U_g = t1^jl t2^kl over (jl, kl) = (g / 3, g % 3), and tile 3 holds the
 // three (il, 2, 2) columns as W[g] = t0^g t1^2 t2^2.
+#ifndef F8_RING
+#define F8_RING 3
+#endif
+__device__ __forceinline__ void cp_async16_sm(void* dst, const void* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 template <int L>
 struct F8Map {
     static_assert(L == 4 || L == 6, "split-exponent spread: L = 4 or 6");
@@ -999,9 +1012,10 @@ struct F8Map {
     static constexpr int MT2 = (L2 + 7) / 8;
     static constexpr int KS2 = (L + 3) / 4;
     static constexpr int LDK = KS2 * 4 + 4;
-    static constexpr int stage = 32 * SR;
+    static constexpr int stage = 32 * SR;      // also the warp's T1 partial at the end
     static constexpr int ph = MT2 * 8 * LDK;
-    static constexpr int area = stage + ph;
+    static constexpr int RING = F8_RING;       // chunks of particle records in flight (cp.async)
+    static constexpr int area = stage + ph + RING * 32 * 4;
     // grid node (i, j, k) of accumulator column `col` at row group g
     __device__ static int node(int g, int col) {
         const int ih = (g >> 2) & 1, jh = (g >> 1) & 1, kh = g & 1;
@@ -1027,9 +1041,15 @@ struct F8Map {
     }
 };
 
+// The warp's T1 partial [MT2*8][RP] reuses the staging rows after the last
+// chunk (MT2*8*RP <= 32*SR for R <= 16; larger R appends it).
+template <int L>
+__host__ __device__ constexpr int spread_f8_t1off(int R) {
+    return F8Map<L>::MT2 * 8 * uv_t1_stride(R) <= F8Map<L>::stage ? 0 : F8Map<L>::area;
+}
 template <int L>
 __host__ __device__ constexpr int spread_f8_warp_doubles(int R) {
-    return F8Map<L>::area + F8Map<L>::MT2 * 8 * uv_t1_stride(R);
+    return F8Map<L>::area + (spread_f8_t1off<L>(R) ? F8Map<L>::MT2 * 8 * uv_t1_stride(R) : 0);
 }
 template <int L>
 __host__ __device__ constexpr size_t spread_f8_smem_doubles(int R, int /*n2*/) {
@@ -1049,11 +1069,12 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_f8(ColumnArgs a, in
     const int per_warp = spread_f8_warp_doubles<L>(R);
     double* St = sm + warp * per_warp;  // [32][SR] staged particle rows
     double* ph = St + M::stage;         // [MT2*8][LDK] finished cell grid
-    double* t1w = St + M::area;         // [MT2*8][RP]  warp partial of T1
+    double4* ring = reinterpret_cast<double4*>(ph + M::ph);  // [RING][32] records, lane-private
+    const int t1off = spread_f8_t1off<L>(R);
+    double* t1w = St + t1off;           // [MT2*8][RP]  warp partial of T1 (after the chunks)
     double* epi = sm + NW * per_warp;   // epilogue scratch
     __shared__ double red[NTH];
     __shared__ int cst[66];
-    for (int e = lane; e < MT2 * 8 * RP; e += 32) t1w[e] = 0.0;
     for (int e = lane; e < M::ph; e += 32) ph[e] = 0.0;  // padding stays zero
     const int col_cell0 = (cr.c0 * g.K[1] + cr.c1) * g.K[2];
     const int nz = cr.ze - cr.zb;
@@ -1093,23 +1114,36 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_f8(ColumnArgs a, in
             zw1 = t0 < t1 ? lb(t1) : cr.zb;
         }
     }
-    // The next chunk's record is loaded one chunk ahead across cell
-    // boundaries (the warp's chunk sequence is cell-aligned), and the one
-    // after that is prefetched into L2.
+    // Particle records stream through a lane-private cp.async ring: the
+    // producer cursor runs RING - 1 chunks ahead of the consumer over the
+    // warp's cell-aligned chunk sequence, across cell boundaries (lane l
+    // copies record l of each chunk; lanes past a chunk's end copy its last
+    // record: finite t, q masked to 0 below).
     auto cell_lo_p = [&](int c) { return max(cstart(c), pw0); };
     auto cell_hi_p = [&](int c) { return min(cstart(c + 1), pw1); };
     int nc2 = zw0, nbase = zw0 < zw1 ? cell_lo_p(zw0) : 0;
-    auto norm = [&](int& c, int& b) {
-        while (c < zw1 && b >= cell_hi_p(c)) {
-            ++c;
-            if (c < zw1) b = cell_lo_p(c);
+    auto norm = [&]() {
+        while (nc2 < zw1 && nbase >= cell_hi_p(nc2)) {
+            ++nc2;
+            if (nc2 < zw1) nbase = cell_lo_p(nc2);
         }
     };
-    norm(nc2, nbase);
-    auto load_at = [&](int c, int b) {
-        return c < zw1 ? ld_rec(a.sp + min(b + lane, cell_hi_p(c) - 1)) : make_double4(0, 0, 0, 0);
+    norm();
+    int pslot = 0, cslot = 0;
+    auto issue = [&]() {
+        if (nc2 < zw1) {
+            const double4* src = a.sp + min(nbase + lane, cell_hi_p(nc2) - 1);
+            double4* dst = ring + pslot * 32 + lane;
+            cp_async16_sm(dst, src);
+            cp_async16_sm(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(src) + 16);
+            nbase += 32;
+            norm();
+        }
+        cp_async_commit();
+        pslot = pslot + 1 == M::RING ? 0 : pslot + 1;
     };
-    double4 nxt = load_at(nc2, nbase);
+#pragma unroll
+    for (int u = 0; u < M::RING - 1; ++u) issue();
     for (int c2 = zw0; c2 < zw1; ++c2) {
         const int s0 = cell_lo_p(c2), s1 = cell_hi_p(c2);
         if (s0 >= s1) {
@@ -1124,12 +1158,10 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_f8(ColumnArgs a, in
         for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
         for (int base = s0; base < s1; base += 32) {
             const int cnt = min(32, s1 - base);
-            const double4 pt = nxt;
-            nbase += 32;
-            norm(nc2, nbase);
-            nxt = load_at(nc2, nbase);
-            if (nc2 < zw1 && nbase + 32 < pw1)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(a.sp + min(nbase + 32 + lane, pw1 - 1)));
+            issue();
+            cp_async_wait<M::RING - 1>();
+            const double4 pt = ring[cslot * 32 + lane];
+            cslot = cslot + 1 == M::RING ? 0 : cslot + 1;
             const double q = lane < cnt ? pt.w : 0.0;
             qsum += q;
             const double t0 = (pt.x - ax0.mid) * ax0.inv;
@@ -1223,7 +1255,10 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_f8(ColumnArgs a, in
         }
         __syncwarp();
     }
+    cp_async_wait<0>();
+    __syncwarp();
     if (want_fwd) {
+        // the rows past MT2*8 stay zero: the epilogue reads only (i, j) < L^2
 #pragma unroll
         for (int mt = 0; mt < MT2; ++mt)
 #pragma unroll
@@ -1236,7 +1271,7 @@ __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_f8(ColumnArgs a, in
     // tensor_weights' out-of-cell check, |t| <= 1 + 2e-12 (slack 1e-12 of the width)
     const unsigned badw = __ballot_sync(0xffffffffu, !(tmax <= 1.0 + 2e-12));
     if (lane == 0 && badw) atomicOr(&a.bad[1], 1ull);
-    spread_epilogue<L, NW>(a, cr, sm, per_warp, M::area, RP, epi, red, qsum, want_fwd);
+    spread_epilogue<L, NW>(a, cr, sm, per_warp, t1off, RP, epi, red, qsum, want_fwd);
 }
 
 // Backward z-expansion + gather with compile-time L: psi for a batch of the

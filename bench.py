@@ -349,7 +349,7 @@ def run_ours(a):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     slab = world > 1 or a.slab
-    if slab and not dist.is_initialized() and "RANK" in os.environ:
+    if (slab or (a.workload == "cfg5" and world > 1)) and not dist.is_initialized() and "RANK" in os.environ:
         dist.init_process_group("nccl", device_id=dev)
     from paper_2601_18838_b200 import inputs
     from paper_2601_18838_b200.plan import KpmePlan
@@ -540,19 +540,19 @@ def extras(torch, dev, flush, steps):
 
 def run_cfg5(a, torch, dist, rank, world, dev):
     """Config 5: the dense SKP grid operator on z-slabs, every mesh and rank
-    of BASELINE (64^3..512^3, R in {4..64}), all three sharded-axis strategies
-    timed per shape (max over ranks, CUDA events, L2 flushed) and the faster
-    one chosen -- the north star's slab all-to-all vs rank-split + reduce,
-    plus the reference's own SPKMV-style reduction (parallel.hpp:169-176).
-    Prints the strategy table on stderr and one JSON line."""
+    of BASELINE (64^3..512^3, R in {4..64}), through the library's slab
+    operator (kpme_gpu_dense_slab: DMMA GEMMs, plan-owned NCCL communicator,
+    preallocated buffers). All three sharded-axis strategies are timed per
+    shape by the library's chooser (CUDA events, max over ranks) and the
+    fastest is kept -- the north star's slab all-to-all vs rank split +
+    reduce, plus the reference's own SPKMV-style reduction
+    (parallel.hpp:169-176). Prints the table on stderr and one JSON line."""
     from paper_2601_18838_b200 import inputs
-    from paper_2601_18838_b200.dist import DenseSlabOperator, slab_bounds
-    from paper_2601_18838_b200.plan import KpmePlan, dgemm_tn
+    from paper_2601_18838_b200.dist import slab_bounds
+    from paper_2601_18838_b200.plan import DenseSlab, KpmePlan, nccl_unique_id
 
     meshes = [int(v) for v in (a.cfg5_meshes or "64,128,256,512").split(",")]
     ranks = [int(v) for v in (a.cfg5_ranks or "4,8,16,32,64").split(",")]
-    flush = torch.empty(FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
-    peaks, _ = load_peaks()
     fp64 = fp64_peak(torch, dev)
     rows = []
     for n in meshes:
@@ -564,25 +564,18 @@ def run_cfg5(a, torch, dist, rank, world, dev):
         g = torch.Generator(device=dev).manual_seed(n)
         x_full = torch.randn(n, n, n, dtype=torch.float64, device=dev, generator=g)
         x_local = x_full[:, :, lo:hi].contiguous()
+        y_local = torch.empty_like(x_local)
         del x_full
         for R in ranks:
             ops = [o[:R].contiguous() for o in ops_all]
-            op = DenseSlabOperator(*ops, (n, n, n), lambda i, f, o, acc: dgemm_tn(i, f, o, acc))
-            tms = {}
-            for s in DenseSlabOperator.STRATEGIES:
-                op.apply(x_local, s)
-                torch.cuda.synchronize()
-                if dist.is_initialized():
-                    dist.barrier()
-                reps = 3 if n <= 256 else 1
-                t = timed_steps(torch, lambda: op.apply(x_local, s), reps, flush)
-                ms = sum(t) / len(t)
-                if dist.is_initialized():
-                    tt = torch.tensor([ms], device=dev)
-                    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                    ms = float(tt.item())
-                tms[s] = ms
-            best = min(tms, key=tms.get)
+            uid = None
+            if world > 1:
+                box = [nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(box, src=0)
+                uid = box[0]
+            op = DenseSlab(*ops, nranks=world, rank=rank, nccl_id=uid)
+            tms, best = op.choose(x_local, y_local, reps=3 if n <= 256 else 1)
+            op.close()
             flops = 6.0 * R * n ** 4
             rows.append({"n": n, "R": R, "ms": tms, "chosen": best,
                          "mesh_gflops": flops / (tms[best] * 1e-3) / 1e9,
@@ -591,7 +584,7 @@ def run_cfg5(a, torch, dist, rank, world, dev):
                 sys.stderr.write(f"cfg5 n={n:4d} R={R:3d} " + " ".join(
                     f"{k}={v:9.3f}ms" for k, v in tms.items()) + f"  -> {best}\n")
             del op, ops
-        del ops_all, x_local
+        del ops_all, x_local, y_local
         torch.cuda.empty_cache()
     if rank == 0:
         head = max(rows, key=lambda r: (r["n"], r["R"]))
@@ -602,6 +595,11 @@ def run_cfg5(a, torch, dist, rank, world, dev):
                 "dtype": "f64", "data": "synthetic (N(0,1) mesh, factors from the SKP "
                                          "construction, BASELINE config 5)",
                 "config": {"workload": "cfg5", "mesh": [head["n"]] * 3, "skp_terms": head["R"]},
+                "impl_config": {"path": "kpme_gpu_dense_slab (library: DMMA GEMMs, NCCL "
+                                        "collectives, chooser)",
+                                "timing": "library CUDA events per apply, max over ranks; "
+                                          "L2 not flushed between reps (meshes >= 256^3 "
+                                          "exceed L2)"},
                 "strategies": rows, "fp64_dgemm_tflops": fp64,
                 "flops_formula": "6 R n^4 (op_count_estimate x2, kron.hpp:201-211)"}
         emit(line)

@@ -268,6 +268,48 @@ int kpme_gpu_dgemm_tn(void* stream, int64_t M, int64_t N, int64_t K,
                       const double* d_in, const double* d_F, double* d_out,
                       int accumulate);
 
+/* ---- dense operator on z-slabs (config 5, multi-GPU) --------------------- */
+/* y = sum_r (A_r (x) B_r (x) C_r) x with x, y distributed as z-slabs
+ * [n0][n1][z_hi - z_lo] (rank order = z order, balanced split of n2; see
+ * kpme_gpu_dense_slab_bounds). The three strategies for the sharded z
+ * product (the reference's axis-group reduction, parallel.hpp:169-176, and
+ * the north star's slab all-to-all and rank split + reduce); every local
+ * product is the FP64 DMMA GEMM. */
+enum {
+    KPME_GPU_SLAB_REDUCE_SCATTER = 0, /* z contracted from the local slice, one reduce-scatter */
+    KPME_GPU_SLAB_RANK_SPLIT = 1,     /* all-gather, terms split over ranks, reduce-scatter   */
+    KPME_GPU_SLAB_ALLTOALL = 2        /* all-to-all z <-> x transpose around the z product      */
+};
+typedef struct kpme_gpu_dense_slab_s* kpme_gpu_dense_slab;
+/* Rank `rank` of an nranks-process job on `device`; A, B, C: the full
+ * [nterms][n][n] operands in that device's memory; nccl_id: 128 bytes from
+ * kpme_gpu_nccl_unique_id on rank 0 (NULL when nranks == 1). The handle owns
+ * its NCCL communicator, streams and every work buffer. */
+int kpme_gpu_dense_slab_create(int device, int n0, int n1, int n2, int nterms,
+                               const double* A, const double* B, const double* C,
+                               int nranks, int rank, const void* nccl_id,
+                               kpme_gpu_dense_slab* out);
+/* All nranks ranks in this process, rank r on devices[r] (devices may
+ * repeat); collectives by peer copies in rank order. A/B/C: per-rank device
+ * pointers. */
+int kpme_gpu_dense_slab_create_group(int nranks, const int* devices, int n0, int n1,
+                                     int n2, int nterms, const double* const* A,
+                                     const double* const* B, const double* const* C,
+                                     kpme_gpu_dense_slab* out);
+int kpme_gpu_dense_slab_destroy(kpme_gpu_dense_slab h);
+int kpme_gpu_dense_slab_bounds(kpme_gpu_dense_slab h, int rank, int* z_lo, int* z_hi);
+/* Stream of local rank `local` (0 for a process rank; 0..nranks-1 for a group). */
+int kpme_gpu_dense_slab_set_stream(kpme_gpu_dense_slab h, int local, void* stream);
+/* x_local/y_local: one device pointer per local rank. Stream-ordered on the
+ * handle's streams; kpme_gpu_dense_slab_sync waits for them. */
+int kpme_gpu_dense_slab_apply(kpme_gpu_dense_slab h, int strategy,
+                              const double* const* x_local, double* const* y_local);
+int kpme_gpu_dense_slab_sync(kpme_gpu_dense_slab h);
+/* Times every strategy (CUDA events, reps applications each, max over
+ * ranks) and returns the fastest in *best; ms[3] gets the per-apply times. */
+int kpme_gpu_dense_slab_choose(kpme_gpu_dense_slab h, const double* const* x_local,
+                               double* const* y_local, int reps, double* ms, int* best);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

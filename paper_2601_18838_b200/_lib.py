@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(HERE, "libkpme_b200.so")
 OK, INVALID_ARGUMENT, RUNTIME, NUMERICAL, CUDA, NCCL = range(6)
 FORM_AUTO, FORM_COLLAPSED, FORM_DENSE = 0, 1, 2
 COLL_AUTO, COLL_PEER, COLL_NCCL = 0, 1, 2
+SLAB_STRATEGIES = ("reduce_scatter", "rank_split", "alltoall")  # KPME_GPU_SLAB_* order
 NCCL_ID_BYTES = 128
 ABI_VERSION = 2
 DEFER_CHECKS = 1
@@ -112,6 +113,20 @@ def _load():
         "kpme_gpu_plan_devices": (C.c_int, [P, C.POINTER(C.c_int), C.c_int]),
         "kpme_gpu_nccl_unique_id": (C.c_int, [C.c_void_p]),
         "kpme_gpu_plan_attach_comm": (C.c_int, [P, C.c_int, C.c_int, C.c_void_p]),
+        "kpme_gpu_dense_slab_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                 P, P, P, C.c_int, C.c_int, C.c_void_p,
+                                                 C.POINTER(P)]),
+        "kpme_gpu_dense_slab_create_group": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_int,
+                                                       C.c_int, C.c_int, C.c_int, C.POINTER(P),
+                                                       C.POINTER(P), C.POINTER(P), C.POINTER(P)]),
+        "kpme_gpu_dense_slab_destroy": (C.c_int, [P]),
+        "kpme_gpu_dense_slab_bounds": (C.c_int, [P, C.c_int, C.POINTER(C.c_int),
+                                                 C.POINTER(C.c_int)]),
+        "kpme_gpu_dense_slab_set_stream": (C.c_int, [P, C.c_int, P]),
+        "kpme_gpu_dense_slab_apply": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(P)]),
+        "kpme_gpu_dense_slab_sync": (C.c_int, [P]),
+        "kpme_gpu_dense_slab_choose": (C.c_int, [P, C.POINTER(P), C.POINTER(P), C.c_int,
+                                                 C.POINTER(C.c_double), C.POINTER(C.c_int)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -142,6 +157,10 @@ EXPORTS = sorted(
         "kpme_gpu_apply_cache_clear", "kpme_gpu_plan_create_multi",
         "kpme_gpu_plan_set_collective", "kpme_gpu_plan_collective", "kpme_gpu_plan_devices",
         "kpme_gpu_nccl_unique_id", "kpme_gpu_plan_attach_comm",
+        "kpme_gpu_dense_slab_create", "kpme_gpu_dense_slab_create_group",
+        "kpme_gpu_dense_slab_destroy", "kpme_gpu_dense_slab_bounds",
+        "kpme_gpu_dense_slab_set_stream", "kpme_gpu_dense_slab_apply", "kpme_gpu_dense_slab_sync",
+        "kpme_gpu_dense_slab_choose",
     ]
 )
 

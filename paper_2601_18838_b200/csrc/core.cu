@@ -171,13 +171,23 @@ __global__ void k_core_sum(int nblocks, int E, const double* __restrict__ Fpart,
     const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (e >= E) return;
     const double* row = Fpart + (int64_t)e * nblocks;
+    // lane sums blocks lane + 64k (s0) and lane + 32 + 64k (s1) in increasing
+    // k; 8 rounds of loads are issued before they are added (latency-bound)
     double s0 = 0.0, s1 = 0.0;
-    int b = lane;
-    for (; b + 32 < nblocks; b += 64) {
-        s0 += row[b];
-        s1 += row[b + 32];
+    for (int b0 = lane; b0 < nblocks; b0 += 64 * 8) {
+        double v0[8], v1[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int b = b0 + 64 * u;
+            v0[u] = b < nblocks ? __ldg(row + b) : 0.0;
+            v1[u] = b + 32 < nblocks ? __ldg(row + b + 32) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            s0 += v0[u];
+            s1 += v1[u];
+        }
     }
-    if (b < nblocks) s0 += row[b];
     double s = s0 + s1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);

@@ -161,27 +161,30 @@ __global__ void k_sum_splits(int64_t E, int splits, const double* __restrict__ p
     }
 }
 
-// Ccat[z'][r * n2 + z] = C_r[z'][z]: the term-concatenated last-pass operand.
-__global__ void k_concat_terms(int nterms, int n, const double* __restrict__ C,
-                               double* __restrict__ Ccat) {
-    const int64_t total = (int64_t)nterms * n * n;
+// Ccat[z'][r * nzi + z] = C_r[z'][coff + z] (z' < n2o, C_r row stride ldc):
+// the term-concatenated last-pass operand (a column slice of C for slabs).
+__global__ void k_concat_terms(int nterms, int n2o, int nzi, int ldc, int coff,
+                               const double* __restrict__ C, double* __restrict__ Ccat) {
+    const int64_t total = (int64_t)nterms * n2o * nzi;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int z = (int)(e % n), zp = (int)((e / n) % n), r = (int)(e / ((int64_t)n * n));
-        Ccat[(int64_t)zp * nterms * n + (int64_t)r * n + z] = C[e];
+        const int z = (int)(e % nzi), zp = (int)((e / nzi) % n2o), r = (int)(e / ((int64_t)nzi * n2o));
+        Ccat[(int64_t)zp * nterms * nzi + (int64_t)r * nzi + z] =
+            C[((int64_t)r * n2o + zp) * ldc + coff + z];
     }
 }
 
-// Ccat[k][z'][r' n2 + z] = C_{k tps + r'}[z'][z]: the term-concatenated
+// Ccat[k][z'][r' nzi + z] = C_{k tps + r'}[z'][coff + z]: the term-concatenated
 // last-pass operand of every split k (tps terms each) in one launch.
-__global__ void k_concat_splits(int nterms, int tps, int n, const double* __restrict__ C,
-                                double* __restrict__ Ccat) {
-    const int64_t total = (int64_t)nterms * n * n;
+__global__ void k_concat_splits(int nterms, int tps, int n2o, int nzi, int ldc, int coff,
+                                const double* __restrict__ C, double* __restrict__ Ccat) {
+    const int64_t total = (int64_t)nterms * n2o * nzi;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int z = (int)(e % n), zp = (int)((e / n) % n), r = (int)(e / ((int64_t)n * n));
+        const int z = (int)(e % nzi), zp = (int)((e / nzi) % n2o), r = (int)(e / ((int64_t)nzi * n2o));
         const int k = r / tps, rl = r % tps;
-        Ccat[(int64_t)k * tps * n * n + (int64_t)zp * tps * n + (int64_t)rl * n + z] = C[e];
+        Ccat[(int64_t)k * tps * n2o * nzi + (int64_t)zp * tps * nzi + (int64_t)rl * nzi + z] =
+            C[((int64_t)r * n2o + zp) * ldc + coff + z];
     }
 }
 
@@ -243,56 +246,68 @@ void dgemm_tn_batched(cudaStream_t s, int64_t M, int64_t N, int64_t K, const dou
     KB_CHECK_LAUNCH();
 }
 
+size_t kron_local_workspace_bytes(int n0, int n1, int nzi, int n2o, int nterms) {
+    const size_t mi = (size_t)n0 * n1 * nzi, mo = (size_t)n0 * n1 * n2o;
+    const int c = chunk_terms(n0, n1, std::max(nzi, n2o), nterms);
+    const int sp = splits_for(n0, n1, n2o, c);
+    return sizeof(double) * (mi * 2 * (size_t)c + (sp > 1 ? mo * sp : 0) + (size_t)n2o * nzi * c) + 256;
+}
+
 size_t dense_workspace_bytes(int n0, int n1, int n2, int nterms) {
-    const size_t mesh = (size_t)n0 * n1 * n2;
-    const int c = chunk_terms(n0, n1, n2, nterms);
-    const int sp = splits_for(n0, n1, n2, c);
-    return sizeof(double) * (mesh * (2 * (size_t)c + (sp > 1 ? sp : 0)) + (size_t)n2 * n2 * c) + 256;
+    return kron_local_workspace_bytes(n0, n1, n2, n2, nterms);
+}
+
+void kron_local(cudaStream_t s, int n0, int n1, int nzi, int n2o, int nterms, const double* A,
+                const double* B, const double* C, int ldc, int coff, const double* x, double* y,
+                bool accumulate, double* work, size_t work_bytes) {
+    const int64_t mi = (int64_t)n0 * n1 * nzi, mo = (int64_t)n0 * n1 * n2o;
+    if (nterms <= 0 || nzi <= 0) {
+        if (!accumulate) KB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * mo, s));
+        return;
+    }
+    const int chunk = chunk_terms(n0, n1, std::max(nzi, n2o), nterms);
+    const int splits = splits_for(n0, n1, n2o, chunk);
+    if (work_bytes < kron_local_workspace_bytes(n0, n1, nzi, n2o, nterms))
+        throw Error(KPME_GPU_INVALID_ARGUMENT, "kron_matvec_dense: workspace too small");
+    double* t1 = work;                          // [chunk][n1][nzi][n0]
+    double* t2 = t1 + mi * chunk;               // [chunk][nzi][n0][n1]
+    double* ccat = t2 + mi * chunk;             // [n2o][chunk * nzi]
+    double* part = ccat + (int64_t)n2o * nzi * chunk;  // [splits][n0 n1][n2o]
+    for (int r0 = 0; r0 < nterms; r0 += chunk) {
+        const int cr = std::min(chunk, nterms - r0);
+        const bool acc = accumulate || r0 > 0;
+        // pass A, all terms of the chunk in one launch: t1_r = x ^T-contracted with A_r
+        dgemm_tn_batched(s, (int64_t)n1 * nzi, n0, n0, x, 0, A + (int64_t)r0 * n0 * n0,
+                         (int64_t)n0 * n0, t1, mi, cr, false);
+        // pass B: t2_r[(z,x')][y'] = sum_y t1_r[y][(z,x')] B_r[y'][y]
+        dgemm_tn_batched(s, (int64_t)nzi * n0, n1, n1, t1, mi, B + (int64_t)r0 * n1 * n1,
+                         (int64_t)n1 * n1, t2, mi, cr, false);
+        // pass C over (term, z): y[(x',y')][z'] (+)= sum_{r,z} t2[r][z][(x',y')] C_r[z'][coff + z]
+        const double* Cr = C + (int64_t)r0 * n2o * ldc;
+        const int sp = even_splits(splits, cr);
+        if (sp <= 1) {
+            k_concat_terms<<<sm_count() * 4, 256, 0, s>>>(cr, n2o, nzi, ldc, coff, Cr, ccat);
+            KB_CHECK_LAUNCH();
+            dgemm_tn(s, (int64_t)n0 * n1, n2o, (int64_t)cr * nzi, t2, ccat, y, acc);
+        } else {
+            // split-K over terms, one batched launch: split k covers terms
+            // [k tps, (k+1) tps) with its concatenated operand [z'][tps nzi]
+            // at ccat + k tps n2o nzi; partial sums summed in split order below
+            const int tps = cr / sp;
+            k_concat_splits<<<sm_count() * 4, 256, 0, s>>>(cr, tps, n2o, nzi, ldc, coff, Cr, ccat);
+            KB_CHECK_LAUNCH();
+            dgemm_tn_batched(s, (int64_t)n0 * n1, n2o, (int64_t)tps * nzi, t2, tps * mi, ccat,
+                             (int64_t)tps * n2o * nzi, part, mo, sp, false);
+            k_sum_splits<<<sm_count() * 8, 256, 0, s>>>(mo, sp, part, y, acc ? 1 : 0);
+            KB_CHECK_LAUNCH();
+        }
+    }
 }
 
 void kron_matvec_dense(cudaStream_t s, int n0, int n1, int n2, int nterms, const double* A,
                        const double* B, const double* C, const double* x, double* y, double* work,
                        size_t work_bytes) {
-    const int64_t mesh = (int64_t)n0 * n1 * n2;
-    if (nterms <= 0) {
-        KB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * mesh, s));
-        return;
-    }
-    const int chunk = chunk_terms(n0, n1, n2, nterms);
-    const int splits = splits_for(n0, n1, n2, chunk);
-    if (work_bytes < dense_workspace_bytes(n0, n1, n2, nterms))
-        throw Error(KPME_GPU_INVALID_ARGUMENT, "kron_matvec_dense: workspace too small");
-    double* t1 = work;                          // [chunk][n1][n2][n0]
-    double* t2 = t1 + mesh * chunk;             // [chunk][n2][n0][n1]
-    double* ccat = t2 + mesh * chunk;           // [n2][chunk * n2]
-    double* part = ccat + (int64_t)n2 * n2 * chunk;  // [splits][n0 n1][n2]
-    for (int r0 = 0; r0 < nterms; r0 += chunk) {
-        const int cr = std::min(chunk, nterms - r0);
-        // pass A, all terms of the chunk in one launch: t1_r = x ^T-contracted with A_r
-        dgemm_tn_batched(s, (int64_t)n1 * n2, n0, n0, x, 0, A + (int64_t)r0 * n0 * n0,
-                         (int64_t)n0 * n0, t1, mesh, cr, false);
-        // pass B: t2_r[(z,x')][y'] = sum_y t1_r[y][(z,x')] B_r[y'][y]
-        dgemm_tn_batched(s, (int64_t)n2 * n0, n1, n1, t1, mesh, B + (int64_t)r0 * n1 * n1,
-                         (int64_t)n1 * n1, t2, mesh, cr, false);
-        // pass C over (term, z): y[(x',y')][z'] (+)= sum_{r,z} t2[r][z][(x',y')] C_r[z'][z]
-        const int sp = even_splits(splits, cr);
-        if (sp <= 1) {
-            k_concat_terms<<<sm_count() * 4, 256, 0, s>>>(cr, n2, C + (int64_t)r0 * n2 * n2, ccat);
-            KB_CHECK_LAUNCH();
-            dgemm_tn(s, (int64_t)n0 * n1, n2, (int64_t)cr * n2, t2, ccat, y, r0 > 0);
-        } else {
-            // split-K over terms, one batched launch: split k covers terms
-            // [k tps, (k+1) tps) with its concatenated operand [z'][tps n2]
-            // at ccat + k tps n2^2; partial sums summed in split order below
-            const int tps = cr / sp;
-            k_concat_splits<<<sm_count() * 4, 256, 0, s>>>(cr, tps, n2, C + (int64_t)r0 * n2 * n2, ccat);
-            KB_CHECK_LAUNCH();
-            dgemm_tn_batched(s, (int64_t)n0 * n1, n2, (int64_t)tps * n2, t2, tps * mesh, ccat,
-                             (int64_t)tps * n2 * n2, part, mesh, sp, false);
-            k_sum_splits<<<sm_count() * 8, 256, 0, s>>>(mesh, sp, part, y, r0 > 0 ? 1 : 0);
-            KB_CHECK_LAUNCH();
-        }
-    }
+    kron_local(s, n0, n1, n2, n2, nterms, A, B, C, n2, 0, x, y, false, work, work_bytes);
 }
 
 }  // namespace kb

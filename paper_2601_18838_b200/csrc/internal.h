@@ -218,7 +218,18 @@ void launch_cells_to_mesh(const Geometry& g, const double* src, double* dst, boo
 // ---- dense.cu ---------------------------------------------------------------
 void dgemm_tn(cudaStream_t s, int64_t M, int64_t N, int64_t K, const double* in,
               const double* F, double* out, bool accumulate);
+// batch entries z: in + z sin, F + z sF, out + z sout
+void dgemm_tn_batched(cudaStream_t s, int64_t M, int64_t N, int64_t K, const double* in,
+                      int64_t sin, const double* F, int64_t sF, double* out, int64_t sout,
+                      int batch, bool accumulate);
 size_t dense_workspace_bytes(int n0, int n1, int n2, int nterms);
+// y[n0 n1][n2o] (+)= sum_r (A_r (x) B_r (x) C_r[:, coff : coff + nzi]) x[n0][n1][nzi]
+// (C_r row-major [n2o][ldc]): the dense operator with a column slice of the
+// last factor -- one z-slab's contribution to every output plane.
+size_t kron_local_workspace_bytes(int n0, int n1, int nzi, int n2o, int nterms);
+void kron_local(cudaStream_t s, int n0, int n1, int nzi, int n2o, int nterms, const double* A,
+                const double* B, const double* C, int ldc, int coff, const double* x, double* y,
+                bool accumulate, double* work, size_t work_bytes);
 void kron_matvec_dense(cudaStream_t s, int n0, int n1, int n2, int nterms, const double* A,
                        const double* B, const double* C, const double* x, double* y,
                        double* work, size_t work_bytes);

@@ -334,6 +334,97 @@ def kron_matvec_dense(A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, x: tor
     return out
 
 
+class DenseSlab:
+    """Config 5 on z-slabs through the library (kpme_gpu_dense_slab_*): the
+    dense operator y = sum_r (A_r (x) B_r (x) C_r) x with x, y as z-slabs
+    [n0][n1][z_hi - z_lo], one rank per GPU, the three sharded-axis
+    strategies (``_lib.SLAB_STRATEGIES``) on the DMMA GEMM with the library's
+    own NCCL communicator and preallocated buffers.
+
+    ``DenseSlab(A, B, C, nranks, rank, nccl_id)``: this process's rank
+    (A, B, C: full [nterms][n][n] operands on its GPU).
+    ``DenseSlab.group(ops_per_rank, devices)``: every rank in this process
+    (devices may repeat; collectives by peer copies in rank order)."""
+
+    def __init__(self, A=None, B=None, C_=None, nranks: int = 1, rank: int = 0,
+                 nccl_id: bytes | None = None, _group=None):
+        self._h = C.c_void_p()
+        if _group is not None:
+            ops, devices = _group
+            self.local = len(devices)
+            self.nranks, self.devices = len(devices), list(devices)
+            A0 = ops[0][0]
+            self.shape = (A0.shape[1], ops[0][1].shape[1], ops[0][2].shape[1])
+            self.nterms = A0.shape[0]
+            self._keep = [o.contiguous() for trio in ops for o in trio]
+            P = C.c_void_p
+            arr = lambda k: (P * self.nranks)(*[_ptr(ops[r][k].contiguous()) for r in range(self.nranks)])
+            self._arrs = [arr(0), arr(1), arr(2)]
+            dv = (C.c_int * self.nranks)(*self.devices)
+            check(lib.kpme_gpu_dense_slab_create_group(self.nranks, dv, *self.shape, self.nterms,
+                                                       *self._arrs, C.byref(self._h)))
+        else:
+            self.local, self.nranks = 1, int(nranks)
+            self.devices = [A.device.index or 0]
+            self.shape = (A.shape[1], B.shape[1], C_.shape[1])
+            self.nterms = A.shape[0]
+            self._keep = [A.contiguous(), B.contiguous(), C_.contiguous()]
+            buf = None
+            if nccl_id is not None:
+                buf = C.create_string_buffer(bytes(nccl_id), _lib.NCCL_ID_BYTES)
+            with torch.cuda.device(self.devices[0]):
+                check(lib.kpme_gpu_dense_slab_create(self.devices[0], *self.shape, self.nterms,
+                                                     *[_ptr(t) for t in self._keep], self.nranks,
+                                                     int(rank), buf, C.byref(self._h)))
+        self.rank = int(rank)
+
+    @classmethod
+    def group(cls, ops_per_rank, devices):
+        return cls(_group=(ops_per_rank, devices))
+
+    def bounds(self, rank: int):
+        lo, hi = C.c_int(), C.c_int()
+        check(lib.kpme_gpu_dense_slab_bounds(self._h, int(rank), C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
+    def _ptrs(self, ts):
+        return (C.c_void_p * len(ts))(*[_ptr(t) for t in ts])
+
+    def apply(self, x_local, y_local, strategy: str = "reduce_scatter", sync: bool = True):
+        """x_local, y_local: one tensor per local rank (lists), or a tensor."""
+        xs = x_local if isinstance(x_local, (list, tuple)) else [x_local]
+        ys = y_local if isinstance(y_local, (list, tuple)) else [y_local]
+        torch.cuda.synchronize()
+        check(lib.kpme_gpu_dense_slab_apply(self._h, _lib.SLAB_STRATEGIES.index(strategy),
+                                            self._ptrs(xs), self._ptrs(ys)))
+        if sync:
+            check(lib.kpme_gpu_dense_slab_sync(self._h))
+        return y_local
+
+    def choose(self, x_local, y_local, reps: int = 1):
+        """Per-strategy time (ms per apply, CUDA events, max over ranks) and
+        the fastest strategy for this shape."""
+        xs = x_local if isinstance(x_local, (list, tuple)) else [x_local]
+        ys = y_local if isinstance(y_local, (list, tuple)) else [y_local]
+        torch.cuda.synchronize()
+        ms = (C.c_double * 3)()
+        best = C.c_int()
+        check(lib.kpme_gpu_dense_slab_choose(self._h, self._ptrs(xs), self._ptrs(ys), int(reps), ms,
+                                             C.byref(best)))
+        return {s: ms[i] for i, s in enumerate(_lib.SLAB_STRATEGIES)}, _lib.SLAB_STRATEGIES[best.value]
+
+    def close(self):
+        if self._h:
+            lib.kpme_gpu_dense_slab_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def dense_workspace_bytes(n0: int, n1: int, n2: int, nterms: int) -> int:
     return int(lib.kpme_gpu_dense_workspace_bytes(n0, n1, n2, nterms))
 

@@ -63,11 +63,11 @@ def test_slab_rejects_foreign_particles():
 
 
 def test_dense_strategies_single_rank_on_dmma():
-    """The dense slab operator's three strategies (world = 1) on the DMMA
-    GEMM equal kron_matvec_dense."""
+    """The library's dense slab operator (kpme_gpu_dense_slab, one process
+    rank, no NCCL at nranks = 1): all three strategies equal
+    kron_matvec_dense, and the chooser times every one."""
     from paper_2601_18838_b200 import inputs
-    from paper_2601_18838_b200.dist import DenseSlabOperator
-    from paper_2601_18838_b200.plan import KpmePlan, dgemm_tn, kron_matvec_dense
+    from paper_2601_18838_b200.plan import DenseSlab, KpmePlan, kron_matvec_dense
 
     cfg, grid, L, dec = inputs.dense_case(64, 4)
     plan = KpmePlan(cfg, grid, L, dec, 1)
@@ -75,10 +75,47 @@ def test_dense_strategies_single_rank_on_dmma():
     x = torch.randn(64, 64, 64, dtype=torch.float64, device="cuda",
                     generator=torch.Generator(device="cuda").manual_seed(3))
     ref = kron_matvec_dense(*ops, x)
-    op = DenseSlabOperator(*ops, (64, 64, 64), lambda a, f, o, acc: dgemm_tn(a, f, o, acc))
-    for s in DenseSlabOperator.STRATEGIES:
-        y = op.apply(x, s)
+    op = DenseSlab(*ops)
+    assert op.bounds(0) == (0, 64)
+    for s in ("reduce_scatter", "rank_split", "alltoall"):
+        y = torch.full_like(x, float("nan"))
+        op.apply(x, y, s)
         assert float(torch.linalg.norm(y - ref) / torch.linalg.norm(ref)) <= 1e-13, s
+    ms, best = op.choose(x, torch.empty_like(x))
+    assert set(ms) == {"reduce_scatter", "rank_split", "alltoall"} and best in ms
+
+
+@pytest.mark.parametrize("world,shape,nterms", [(2, (24, 20, 32), 5), (3, (32, 24, 40), 4),
+                                                (4, (20, 16, 26), 7), (5, (40, 16, 23), 3)])
+def test_dense_slab_group_strategies(world, shape, nterms):
+    """`world` ranks of the dense slab operator held by one process on the one
+    B200 (kpme_gpu_dense_slab_create_group: the same local kernels, packing
+    and block layouts as one rank per GPU; the collectives are peer copies in
+    rank order). Uneven z- and x-slabs, rectangular meshes, term counts not a
+    multiple of the rank count: every strategy equals the dense operator
+    (<= 1e-13) on every rank's slab."""
+    from paper_2601_18838_b200.dist import slab_bounds
+    from paper_2601_18838_b200.plan import DenseSlab, kron_matvec_dense
+
+    g = torch.Generator(device="cuda").manual_seed(world)
+    n0, n1, n2 = shape
+    A = torch.randn(nterms, n0, n0, dtype=torch.float64, device="cuda", generator=g)
+    B = torch.randn(nterms, n1, n1, dtype=torch.float64, device="cuda", generator=g)
+    C_ = torch.randn(nterms, n2, n2, dtype=torch.float64, device="cuda", generator=g)
+    x = torch.randn(n0, n1, n2, dtype=torch.float64, device="cuda", generator=g)
+    ref = kron_matvec_dense(A, B, C_, x)
+    op = DenseSlab.group([(A, B, C_)] * world, [0] * world)
+    bounds = [op.bounds(r) for r in range(world)]
+    assert bounds == [slab_bounds(n2, r, world) for r in range(world)]
+    xs = [x[:, :, lo:hi].contiguous() for lo, hi in bounds]
+    for s in ("reduce_scatter", "rank_split", "alltoall"):
+        ys = [torch.full_like(t, float("nan")) for t in xs]
+        op.apply(xs, ys, s)
+        for (lo, hi), y in zip(bounds, ys):
+            r = ref[:, :, lo:hi]
+            assert float(torch.linalg.norm(y - r) / torch.linalg.norm(r)) <= 1e-13, (s, lo, hi)
+    ms, best = op.choose(xs, [torch.empty_like(t) for t in xs])
+    assert best in ms
 
 
 @pytest.mark.parametrize("dims", [(2, 2, 2), (1, 3, 1), (2, 1, 3)])

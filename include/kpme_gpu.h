@@ -108,6 +108,19 @@ int kpme_skp_from_quadrature(int count, const double* nodes,
 int kpme_load_tabulated_rule(const char* path, int cap, int* count,
                              double* nodes, double* weights, double* min_arg,
                              double* max_arg, double* eps);
+/* assemble_alpha (alpha.hpp:54-65): the target tensor alpha(m), entries
+ * [(2M+1)^3], m0 slowest, m = -M..M. */
+int kpme_assemble_alpha(double xi, int modes, double* entries);
+/* nkpa_svd (alpha.hpp:225-281): SVD-kind decomposition of alpha by two nested
+ * truncated SVDs (host one-sided Jacobi). Writes up to cap terms:
+ * term_weights[cap], profiles[cap][3][2M+1]; *nterms = the term count (call
+ * with cap = 0 / NULL arrays to size); error_bound (nullable) = the a priori
+ * Frobenius estimate. Correction is 0 (SkpKind::svd). The plan API consumes
+ * these terms like any other (signed profiles ride on the factors,
+ * symfourier.hpp:101-102). */
+int kpme_nkpa_svd(int modes, const double* alpha, double tol_outer, double tol_inner,
+                  int cap, int* nterms, double* term_weights, double* profiles,
+                  double* error_bound);
 /* sample_cloud (geometry.hpp:238-251), splitmix64. */
 void kpme_sample_cloud(const double center[3], double radius, int64_t n,
                        uint64_t seed, double* xyz, double* q);

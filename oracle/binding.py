@@ -179,6 +179,25 @@ class CpuKpme:
             C.byref(corr)))
         return tw[:cnt], prof[:cnt], corr.value
 
+    # ---- SVD kind (reference back ends only) ----------------------------
+    def assemble_alpha(self, xi, modes):
+        n = 2 * modes + 1
+        out = np.zeros(n ** 3)
+        self._check(self._f("assemble_alpha")(C.c_double(xi), modes, _d(out)))
+        return out
+
+    def nkpa_svd(self, alpha, modes, tol_outer, tol_inner):
+        """(term_weights, profiles[nterms][3][2M+1], error_bound)."""
+        n = 2 * modes + 1
+        alpha = np.ascontiguousarray(alpha, dtype=np.float64)
+        cap = n * n + 1
+        tw, prof = np.zeros(cap), np.zeros((cap, 3, n))
+        cnt, bound = C.c_int(), C.c_double()
+        self._check(self._f("nkpa_svd")(modes, _d(alpha), C.c_double(tol_outer),
+                                        C.c_double(tol_inner), cap, C.byref(cnt), _d(tw),
+                                        _d(prof), C.byref(bound)))
+        return tw[:cnt.value].copy(), prof[:cnt.value].copy(), bound.value
+
     # ---- interpolation / symfourier -------------------------------------
     def lagrange_weights_1d(self, order, a, b, y):
         w = np.zeros(order)

@@ -340,4 +340,34 @@ int kr_dense_reciprocal_apply(std::int64_t n, const double* pos, const double* q
     });
 }
 
+// assemble_alpha (alpha.hpp:54-65) and nkpa_svd (alpha.hpp:225-281): the
+// SVD-kind decomposition the GPU library's kpme_nkpa_svd is pinned against.
+int kr_assemble_alpha(double xi, int modes, double* entries) {
+    return guarded([&] {
+        const AlphaVector a = assemble_alpha(EwaldConfig(xi, modes));
+        for (Eigen::Index i = 0; i < a.entries.size(); ++i) entries[i] = a.entries(i);
+    });
+}
+
+int kr_nkpa_svd(int modes, const double* alpha, double tol_outer, double tol_inner, int cap,
+                int* nterms, double* term_weights, double* profiles, double* error_bound) {
+    return guarded([&] {
+        const int n = 2 * modes + 1;
+        AlphaVector a;
+        a.modes = modes;
+        a.entries = Eigen::VectorXd(std::int64_t(n) * n * n);
+        for (std::int64_t i = 0; i < std::int64_t(n) * n * n; ++i) a.entries(i) = alpha[i];
+        double bound = 0.0;
+        const SkpDecomposition dec = nkpa_svd(a, tol_outer, tol_inner, &bound);
+        *nterms = int(dec.terms.size());
+        if (error_bound) *error_bound = bound;
+        for (int t = 0; t < *nterms && t < cap; ++t) {
+            term_weights[t] = dec.terms[t].weight;
+            for (int ax = 0; ax < 3; ++ax)
+                for (int m = 0; m < n; ++m)
+                    profiles[(std::int64_t(t) * 3 + ax) * n + m] = dec.terms[t].profiles[ax](m);
+        }
+    });
+}
+
 }  // extern "C"

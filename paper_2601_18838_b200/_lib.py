@@ -76,6 +76,9 @@ def _load():
         "kpme_load_tabulated_rule": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_int), _dp,
                                                _dp, _dp, _dp, _dp]),
         "kpme_sample_cloud": (None, [_dp, C.c_double, C.c_int64, C.c_uint64, _dp, _dp]),
+        "kpme_assemble_alpha": (C.c_int, [C.c_double, C.c_int, _dp]),
+        "kpme_nkpa_svd": (C.c_int, [C.c_int, _dp, C.c_double, C.c_double, C.c_int,
+                                    C.POINTER(C.c_int), _dp, _dp, _dp]),
         "kpme_gpu_ledger": (C.c_int, [C.POINTER(Config), _i64p, C.c_int64, _i64p]),
         "kpme_gpu_apply": (C.c_int, [C.POINTER(Config), C.c_int64, _dp, _dp, _dp]),
         "kpme_gpu_plan_create": (C.c_int, [C.POINTER(Config), C.c_int64, C.POINTER(P)]),
@@ -160,7 +163,7 @@ EXPORTS = sorted(
         "kpme_gpu_dense_slab_create", "kpme_gpu_dense_slab_create_group",
         "kpme_gpu_dense_slab_destroy", "kpme_gpu_dense_slab_bounds",
         "kpme_gpu_dense_slab_set_stream", "kpme_gpu_dense_slab_apply", "kpme_gpu_dense_slab_sync",
-        "kpme_gpu_dense_slab_choose",
+        "kpme_gpu_dense_slab_choose", "kpme_assemble_alpha", "kpme_nkpa_svd",
     ]
 )
 

@@ -262,6 +262,45 @@ def sinc_rule_for_eps(eps: float, modes: int, max_n: int = 400) -> QuadratureRul
                           3.0 * modes * modes, e.value)
 
 
+@dataclass
+class AlphaVector:
+    """alpha.hpp:42-52: alpha(m) on [-M, M]^3, m0 slowest."""
+
+    modes: int
+    entries: np.ndarray
+
+    def at(self, m0: int, m1: int, m2: int) -> float:
+        n = 2 * self.modes + 1
+        return float(self.entries[((m0 + self.modes) * n + (m1 + self.modes)) * n
+                                  + (m2 + self.modes)])
+
+
+def assemble_alpha(cfg: EwaldConfig) -> AlphaVector:
+    """alpha.hpp:54-65."""
+    n = 2 * cfg.modes + 1
+    out = np.zeros(n ** 3)
+    check(lib.kpme_assemble_alpha(cfg.xi, cfg.modes, _d(out)))
+    return AlphaVector(cfg.modes, out)
+
+
+def nkpa_svd(alpha: AlphaVector, tol_outer: float, tol_inner: float):
+    """nkpa_svd (alpha.hpp:225-281): SVD-kind SkpDecomposition of alpha by two
+    nested truncated SVDs, and the a priori error bound. Raises ValueError
+    for tol_inner > tol_outer (std::invalid_argument in the reference)."""
+    n = 2 * alpha.modes + 1
+    a = np.ascontiguousarray(alpha.entries, dtype=np.float64)
+    cnt, bound = C.c_int(), C.c_double()
+    check(lib.kpme_nkpa_svd(alpha.modes, _d(a), tol_outer, tol_inner, 0, C.byref(cnt), None, None,
+                            C.byref(bound)))
+    cap = max(cnt.value, 1)
+    tw, prof = np.zeros(cap), np.zeros((cap, 3, n))
+    check(lib.kpme_nkpa_svd(alpha.modes, _d(a), tol_outer, tol_inner, cap, C.byref(cnt), _d(tw),
+                            _d(prof), C.byref(bound)))
+    terms = [SkpTerm(float(tw[i]), (prof[i, 0].copy(), prof[i, 1].copy(), prof[i, 2].copy()))
+             for i in range(cnt.value)]
+    return SkpDecomposition(SkpKind.svd, alpha.modes, 0.0, terms), bound.value
+
+
 def skp_from_quadrature(rule: QuadratureRule, cfg: EwaldConfig,
                         kind: SkpKind = SkpKind.sinc) -> SkpDecomposition:
     """alpha.hpp:165-188."""

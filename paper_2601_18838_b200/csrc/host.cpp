@@ -4,6 +4,7 @@
 // (parallel.hpp:84-145). None of this is on the device path; kpme_apply
 // callers normally build the decomposition once, outside the timed call
 // (tools/kpme.cpp:64-77).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -215,5 +216,177 @@ extern "C" int kpme_gpu_ledger(const kpme_gpu_config* cfg, int64_t* out, int64_t
                     for (int64_t r = 0; r < ncell; ++r) push(r, step, p, payload);
         }
         *rows = k;
+    });
+}
+
+// ---- SVD-kind decompositions (alpha.hpp:42-65, 214-281) -------------------
+
+namespace {
+
+// alpha_weight (alpha.hpp:34-39): exp(-pi^2 |m|^2 / xi^2) / |m|^2, 0 at m = 0.
+double alpha_at(double xi, int m0, int m1, int m2) {
+    const double r2 = double(m0) * m0 + double(m1) * m1 + double(m2) * m2;
+    if (r2 == 0.0) return 0.0;
+    const double p = M_PI / xi;
+    return std::exp(-p * p * r2) / r2;
+}
+
+// Thin SVD a = U diag(s) V^T of a row-major m x n matrix by one-sided
+// (Hestenes) Jacobi rotations on the columns of the taller orientation;
+// k = min(m, n) singular values, descending. U: m x k, V: n x k, row-major.
+// Signs: each pair (U_j, V_j) is flipped so that the largest-magnitude entry
+// of V_j is positive (the product U_j s_j V_j^T is sign-free).
+void jacobi_svd(int m, int n, const std::vector<double>& a, std::vector<double>& U,
+                std::vector<double>& s, std::vector<double>& V) {
+    const bool tall = m >= n;
+    const int r = tall ? m : n, c = tall ? n : m;  // work on r x c, columns rotated
+    std::vector<double> w((size_t)r * c), j((size_t)c * c, 0.0);
+    for (int i = 0; i < r; ++i)
+        for (int k = 0; k < c; ++k) w[(size_t)i * c + k] = tall ? a[(size_t)i * n + k] : a[(size_t)k * n + i];
+    for (int k = 0; k < c; ++k) j[(size_t)k * c + k] = 1.0;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0;
+        for (int p = 0; p < c; ++p)
+            for (int q = p + 1; q < c; ++q) {
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int i = 0; i < r; ++i) {
+                    const double x = w[(size_t)i * c + p], y = w[(size_t)i * c + q];
+                    al += x * x;
+                    be += y * y;
+                    ga += x * y;
+                }
+                if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
+                off = std::max(off, std::abs(ga) / std::sqrt(al * be));
+                const double zeta = (be - al) / (2.0 * ga);
+                const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
+                const double cs = 1.0 / std::sqrt(1.0 + t * t), sn = cs * t;
+                for (int i = 0; i < r; ++i) {
+                    double& x = w[(size_t)i * c + p];
+                    double& y = w[(size_t)i * c + q];
+                    const double xo = x, yo = y;
+                    x = cs * xo - sn * yo;
+                    y = sn * xo + cs * yo;
+                }
+                for (int i = 0; i < c; ++i) {
+                    double& x = j[(size_t)i * c + p];
+                    double& y = j[(size_t)i * c + q];
+                    const double xo = x, yo = y;
+                    x = cs * xo - sn * yo;
+                    y = sn * xo + cs * yo;
+                }
+            }
+        if (off < 1e-15) break;
+    }
+    // column norms = singular values; Q = w / s (r x c), J (c x c)
+    std::vector<double> sv(c);
+    for (int k = 0; k < c; ++k) {
+        double t = 0.0;
+        for (int i = 0; i < r; ++i) t += w[(size_t)i * c + k] * w[(size_t)i * c + k];
+        sv[k] = std::sqrt(t);
+    }
+    std::vector<int> order(c);
+    for (int k = 0; k < c; ++k) order[k] = k;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return sv[x] > sv[y]; });
+    // tall: a = Q S J^T -> U = Q, V = J; wide: a^T = Q S J^T -> U = J, V = Q
+    U.assign((size_t)m * c, 0.0);
+    V.assign((size_t)n * c, 0.0);
+    s.assign(c, 0.0);
+    for (int kk = 0; kk < c; ++kk) {
+        const int k = order[kk];
+        s[kk] = sv[k];
+        std::vector<double> qk(r), jk(c);
+        for (int i = 0; i < r; ++i) qk[i] = sv[k] > 0.0 ? w[(size_t)i * c + k] / sv[k] : 0.0;
+        for (int i = 0; i < c; ++i) jk[i] = j[(size_t)i * c + k];
+        const std::vector<double>& uk = tall ? qk : jk;
+        const std::vector<double>& vk = tall ? jk : qk;
+        int big = 0;
+        for (int i = 1; i < n; ++i)
+            if (std::abs(vk[i]) > std::abs(vk[big])) big = i;
+        const double sg = vk[big] < 0.0 ? -1.0 : 1.0;
+        for (int i = 0; i < m; ++i) U[(size_t)i * c + kk] = sg * uk[i];
+        for (int i = 0; i < n; ++i) V[(size_t)i * c + kk] = sg * vk[i];
+    }
+}
+
+}  // namespace
+
+// assemble_alpha (alpha.hpp:54-65): entries[((m0+M) n + (m1+M)) n + (m2+M)].
+extern "C" int kpme_assemble_alpha(double xi, int modes, double* entries) {
+    return guarded([&] {
+        if (!(xi > 0.0)) throw Error(KPME_GPU_INVALID_ARGUMENT, "EwaldConfig: xi must be positive");
+        if (modes < 1) throw Error(KPME_GPU_INVALID_ARGUMENT, "EwaldConfig: modes must be >= 1");
+        if (!entries) throw Error(KPME_GPU_INVALID_ARGUMENT, "kpme_assemble_alpha: null output");
+        const int M = modes, n = 2 * M + 1;
+        for (int m0 = -M; m0 <= M; ++m0)
+            for (int m1 = -M; m1 <= M; ++m1)
+                for (int m2 = -M; m2 <= M; ++m2)
+                    entries[((size_t)(m0 + M) * n + (m1 + M)) * n + (m2 + M)] = alpha_at(xi, m0, m1, m2);
+    });
+}
+
+// nkpa_svd (alpha.hpp:225-281): two nested truncated SVDs -- the unfolding
+// with axis-0 rows, then each kept right singular vector unfolded with axis-1
+// rows -- keeping singular values > tol * s_max. Terms: weight s_i s_ij,
+// profiles (u_i, u_ij, v_ij) over m = -M..M; correction 0.
+extern "C" int kpme_nkpa_svd(int modes, const double* alpha, double tol_outer, double tol_inner,
+                             int cap, int* nterms, double* term_weights, double* profiles,
+                             double* error_bound) {
+    return guarded([&] {
+        if (tol_inner > tol_outer)
+            throw Error(KPME_GPU_INVALID_ARGUMENT, "nkpa_svd: tol_inner must be <= tol_outer");
+        if (modes < 1 || !alpha || !nterms)
+            throw Error(KPME_GPU_INVALID_ARGUMENT, "kpme_nkpa_svd: bad argument");
+        const int n = 2 * modes + 1;
+        std::vector<double> outer(alpha, alpha + (size_t)n * n * n);  // matricize axis 0: n x n^2
+        std::vector<double> U0, s0, V0;
+        jacobi_svd(n, n * n, outer, U0, s0, V0);
+        double sum0 = 0.0;
+        for (double v : s0) sum0 += v;
+        if (!std::isfinite(sum0))
+            throw Error(KPME_GPU_NUMERICAL, "nkpa_svd: outer SVD produced non-finite values");
+        const int k0 = (int)s0.size();
+        const double s0max = k0 ? s0[0] : 0.0;
+        double bound = 0.0, tail0 = 0.0;
+        int count = 0;
+        for (int i = 0; i < k0; ++i) {
+            if (s0max == 0.0 || s0[i] <= tol_outer * s0max) {
+                tail0 += s0[i] * s0[i];
+                continue;
+            }
+            std::vector<double> inner((size_t)n * n);  // matricize(w, {n, n}, 0)
+            for (int e = 0; e < n * n; ++e) inner[e] = V0[(size_t)e * k0 + i];
+            std::vector<double> U1, s1, V1;
+            jacobi_svd(n, n, inner, U1, s1, V1);
+            double sum1 = 0.0;
+            for (double v : s1) sum1 += v;
+            if (!std::isfinite(sum1))
+                throw Error(KPME_GPU_NUMERICAL, "nkpa_svd: inner SVD produced non-finite values");
+            const int k1 = (int)s1.size();
+            const double s1max = k1 ? s1[0] : 0.0;
+            double tail1 = 0.0;
+            for (int jj = 0; jj < k1; ++jj) {
+                if (s1max == 0.0 || s1[jj] <= tol_inner * s1max) {
+                    tail1 += s1[jj] * s1[jj];
+                    continue;
+                }
+                if (count < cap && term_weights && profiles) {
+                    term_weights[count] = s0[i] * s1[jj];
+                    double* p = profiles + (size_t)count * 3 * n;
+                    for (int m = 0; m < n; ++m) {
+                        p[m] = U0[(size_t)m * k0 + i];
+                        p[n + m] = U1[(size_t)m * k1 + jj];
+                        p[2 * n + m] = V1[(size_t)m * k1 + jj];
+                    }
+                }
+                ++count;
+            }
+            bound += s0[i] * std::sqrt(tail1);
+        }
+        bound += std::sqrt(tail0);
+        *nterms = count;
+        if (error_bound) *error_bound = bound;
+        if (count > cap && term_weights)
+            throw Error(KPME_GPU_INVALID_ARGUMENT, "kpme_nkpa_svd: more terms than cap (" +
+                                                       std::to_string(count) + ")");
     });
 }

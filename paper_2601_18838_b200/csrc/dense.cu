@@ -11,7 +11,11 @@
 // original order: [x][y][z] -A-> [y][z][x'] -B-> [z][x'][y'] -C-> [x'][y'][z'].
 // The last pass contracts over (term, z) at once (K = chunk * n2), so the
 // per-term partial sums accumulate in the DMMA registers.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <mutex>
 
 #include "internal.h"
 
@@ -150,6 +154,165 @@ __global__ void __launch_bounds__(THREADS) k_dgemm_tn(int64_t M, int64_t N, int6
     }
 }
 
+// ---- TMA-staged variant ------------------------------------------------------
+// The same 128 x 64 x 16 CTA tile and warp tiling, with operand tiles staged by
+// the Tensor Memory Accelerator: one cp.async.bulk.tensor per operand per
+// k-tile, issued by one thread, completing on an mbarrier per stage; out-of-
+// range rows/columns arrive as zeros (no predicated per-element copies).
+//   A tile: in[z][k][m], box {128 m, 16 k}, dense [16][128] (row offsets are
+//           multiples of 1 KB, so the fragment reads of 4 k rows are 2-way
+//           conflicted; they are 1/3 of the smem traffic per DMMA)
+//   B tile: F[z][i][k], box {16 k, 64 i}, 128-byte swizzle: the 16-byte chunk
+//           c of row i sits at chunk c ^ (i % 8), so a warp's fragment reads
+//           (8 rows x 2 chunks per k pair) are conflict-free.
+constexpr int TSTAGES = 4;
+constexpr size_t kTmaA = (size_t)BK * BM * sizeof(double);  // 16 KB
+constexpr size_t kTmaB = (size_t)BN * BK * sizeof(double);  // 8 KB
+constexpr size_t kSmemTma = TSTAGES * (kTmaA + kTmaB) + 1024 + 64;
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbarrier_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbarrier_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbarrier_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tTMA_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra TMA_WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS) k_dgemm_tn_tma(int64_t M, int64_t N, int64_t K,
+                                                          const __grid_constant__ CUtensorMap tmA,
+                                                          const __grid_constant__ CUtensorMap tmB,
+                                                          int zA, int zB, double* __restrict__ out,
+                                                          int accumulate, int64_t sout) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // 1024-byte alignment for the 128-byte swizzle
+    unsigned char* base = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    double* As = reinterpret_cast<double*>(base);                       // [S][BK][BM]
+    double* Bs = reinterpret_cast<double*>(base + TSTAGES * kTmaA);     // [S][BN][BK] swizzled
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + TSTAGES * (kTmaA + kTmaB));
+    out += blockIdx.z * sout;
+    const int za = zA ? (int)blockIdx.z : 0, zb = zB ? (int)blockIdx.z : 0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    const int ktiles = (int)((K + BK - 1) / BK);
+    if (tid == 0) {
+        for (int s = 0; s < TSTAGES; ++s) mbarrier_init(full + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int kt) {
+        const int s = kt % TSTAGES;
+        mbarrier_expect_tx(full + s, (unsigned)(kTmaA + kTmaB));
+        tma_load_3d(As + (size_t)s * BK * BM, &tmA, (int)m0, kt * BK, za, full + s);
+        tma_load_3d(Bs + (size_t)s * BN * BK, &tmB, kt * BK, (int)n0, zb, full + s);
+    };
+    if (tid == 0)
+        for (int kt = 0; kt < TSTAGES && kt < ktiles; ++kt) issue(kt);
+
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const int g = lane >> 2, c = lane & 3;
+    for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % TSTAGES;
+        mbarrier_wait(full + s, (unsigned)((kt / TSTAGES) & 1));
+        const double* as = As + (size_t)s * BK * BM + wm * 64 + g;
+        const char* bs = reinterpret_cast<const char*>(Bs + (size_t)s * BN * BK);
+#pragma unroll
+        for (int k4 = 0; k4 < BK; k4 += 4) {
+            double a[8], b[4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = as[(k4 + c) * BM + i * 8];
+            const int kk = k4 + c;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int row = wn * 32 + j * 8 + g;  // row % 8 == g
+                b[j] = *reinterpret_cast<const double*>(
+                    bs + row * 128 + ((((kk >> 1) ^ g) & 7) << 4) + ((kk & 1) << 3));
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+        }
+        __syncthreads();  // stage s fully read
+        if (tid == 0 && kt + TSTAGES < ktiles) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(kt + TSTAGES);
+        }
+    }
+
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t row = m0 + wm * 64 + i * 8 + g;
+        if (row >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t col = n0 + wn * 32 + j * 8 + 2 * c;
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+                if (col + e < N) {
+                    double* o = out + row * N + col + e;
+                    *o = accumulate ? *o + acc[i][j][e] : acc[i][j][e];
+                }
+        }
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+// rows x cols (cols fastest) x batch FP64 tensor; batch stride in elements
+// (0: one matrix broadcast to every batch entry).
+bool make_map(CUtensorMap* map, const double* ptr, int64_t rows, int64_t cols, int64_t bstride,
+              int batch, unsigned box_cols, unsigned box_rows, bool swizzle128) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows,
+                                (cuuint64_t)(bstride ? batch : 1)};
+    const cuuint64_t strides[2] = {(cuuint64_t)cols * 8, (cuuint64_t)(bstride ? bstride : rows * cols) * 8};
+    const cuuint32_t box[3] = {box_cols, box_rows, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptr), dims, strides, box,
+              estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // out[e] (+)= sum_s part[s][e] over splits in order (deterministic split-K).
 __global__ void k_sum_splits(int64_t E, int splits, const double* __restrict__ part,
                              double* __restrict__ out, int accumulate) {
@@ -235,6 +398,29 @@ void dgemm_tn_batched(cudaStream_t s, int64_t M, int64_t N, int64_t K, const dou
     });
     if (M <= 0 || N <= 0 || batch <= 0) return;
     const dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)batch);
+    // TMA path: 16-byte aligned bases and row / batch strides (M, K even)
+    static const bool tma_env = [] {
+        const char* e = getenv("KPME_DGEMM_TMA");
+        return !(e && *e == '0');
+    }();
+    const bool tma_ok = tma_env && (M % 2 == 0) && (K % 2 == 0) && ((uintptr_t)in % 16 == 0) &&
+                        ((uintptr_t)F % 16 == 0) && (sin % 2 == 0) && (sF % 2 == 0) &&
+                        M < (int64_t(1) << 31) && N < (int64_t(1) << 31) && K < (int64_t(1) << 31);
+    if (tma_ok) {
+        CUtensorMap ta, tb;
+        if (make_map(&ta, in, K, M, sin, batch, BM, BK, false) &&
+            make_map(&tb, F, N, K, sF, batch, BK, BN, true)) {
+            static PerDevice tma_once;
+            once_per_device(tma_once, [&] {
+                KB_CUDA(cudaFuncSetAttribute(k_dgemm_tn_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kSmemTma));
+            });
+            k_dgemm_tn_tma<<<grid, THREADS, kSmemTma, s>>>(M, N, K, ta, tb, sin ? 1 : 0, sF ? 1 : 0,
+                                                           out, accumulate ? 1 : 0, sout);
+            KB_CHECK_LAUNCH();
+            return;
+        }
+    }
     const bool vec = (M % 2 == 0) && (K % 2 == 0) && ((uintptr_t)in % 16 == 0) &&
                      ((uintptr_t)F % 16 == 0) && (sin % 2 == 0) && (sF % 2 == 0);
     if (vec)

@@ -990,7 +990,7 @@ __global__ void __launch_bounds__(32 * UV_NW, SPREAD_MINB) k_spread_uv(ColumnArg
 // U_g = t1^jl t2^kl over (jl, kl) = (g / 3, g % 3), and tile 3 holds the
 // three (il, 2, 2) columns as W[g] = t0^g t1^2 t2^2.
 #ifndef F8_RING
-#define F8_RING 3
+#define F8_RING 2
 #endif
 __device__ __forceinline__ void cp_async16_sm(void* dst, const void* src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -1056,8 +1056,12 @@ __host__ __device__ constexpr size_t spread_f8_smem_doubles(int R, int /*n2*/) {
     return 4 * (size_t)spread_f8_warp_doubles<L>(R) + (size_t)spread_epilogue_doubles(L, R);
 }
 
-template <int L, int RTM>
-__global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_f8(ColumnArgs a, int want_fwd) {
+// MINB: CTAs per SM the register allocation is sized for. 3 (162 registers)
+// when the column CTAs make about one wave at three per SM (config 3: 441
+// columns, 45.2 vs 47.6 us at 4); 4 (128 registers, a few spilled bytes) for
+// grids of several waves (config 4: 1849 columns, 173.5 vs 179.8 us).
+template <int L, int RTM, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_fwd) {
     using M = F8Map<L>;
     constexpr int L3 = L * L * L, NT = M::NT, MT2 = M::MT2, KS2 = M::KS2, LDK = M::LDK, SR = M::SR;
     constexpr int NW = 4, NTH = 128;
@@ -1720,16 +1724,21 @@ bool launch_spread_f8_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
         if (!SPREAD_F8 || smem > 200 * 1024 || a.g.R > 32) return false;
         static PerDevice attr_once;
         once_per_device(attr_once, [&] {
-            KB_CUDA(cudaFuncSetAttribute(k_spread_f8<L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            KB_CUDA(cudaFuncSetAttribute(k_spread_f8<L, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          200 * 1024));
-            KB_CUDA(cudaFuncSetAttribute(k_spread_f8<L, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            KB_CUDA(cudaFuncSetAttribute(k_spread_f8<L, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         200 * 1024));
+            KB_CUDA(cudaFuncSetAttribute(k_spread_f8<L, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          200 * 1024));
         });
         const int grid = block_columns(a.g) * a.S;
-        if (a.g.R <= 16)
-            k_spread_f8<L, 2><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+        const bool waves = grid > 2 * 3 * sm_count() && smem * 4 <= 220 * 1024;
+        if (a.g.R <= 16 && waves)
+            k_spread_f8<L, 2, 4><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+        else if (a.g.R <= 16)
+            k_spread_f8<L, 2, 3><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
         else
-            k_spread_f8<L, 4><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+            k_spread_f8<L, 4, 3><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
         KB_CHECK_LAUNCH();
         return true;
     } else {

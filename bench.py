@@ -316,7 +316,7 @@ def stage_rooflines(torch, plan, run_eager, w, n, K, flush, steps, peaks, fp64):
     S = max(1, min(K[2], (3 * 148) // max(1, K[0] * K[1])))
     hbm = peaks["hbm_gbs"]
     out = {}
-    for name, t_ms, (flops, bytes_) in (("k_sort", st[0], sort_algorithmic(n)),
+    for name, t_ms, (flops, bytes_) in (("k_sort_stage", st[0], sort_algorithmic(n)),
                                        ("k_spread_fwd", st[1], spread_algorithmic(w, n, K, S)),
                                        ("k_bwd_gather", st[3], gather_algorithmic(w, n, K))):
         t_hbm = bytes_ / (hbm * 1e9)
@@ -332,6 +332,8 @@ def stage_rooflines(torch, plan, run_eager, w, n, K, flush, steps, peaks, fp64):
             ach = bytes_ / (t_ms * 1e-3) / 1e9
             r = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                  "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        if name == "k_sort_stage":
+            r["kernels"] = "k_tile_sort + k_z_tiles (<= 512 columns) or k_tile_hist + k_col_scan + k_col_scatter + k_z_sort"
         r.update({"kernel": name, "algorithmic_flops": flops, "algorithmic_bytes": bytes_,
                   "kernel_ms": t_ms, "traffic": ncu_traffic(name),
                   "traffic_source": "profiles/ncu_summary.json (ncu --set full of this workload)"})
@@ -430,7 +432,9 @@ def run_ours(a):
     fp64 = fp64_peak(torch, dev)
     stages, rooflines = stage_rooflines(torch, plan, run_eager, w, n_local, K_local, flush,
                                         a.steps, peaks, fp64)
-    dom = max(("k_spread_fwd", "k_bwd_gather", "k_sort"), key=lambda k: rooflines[k]["kernel_ms"])
+    # the dominant single kernel (the sort stage is two kernels; its stage
+    # roofline is reported beside it in `rooflines`)
+    dom = max(("k_spread_fwd", "k_bwd_gather"), key=lambda k: rooflines[k]["kernel_ms"])
     roofline = rooflines[dom]
     meta["fp64_dgemm_tflops"] = fp64
 

@@ -13,7 +13,8 @@ rep, out, desc = sys.argv[1], sys.argv[2], sys.argv[3]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, data = rows[0], rows[2:]
-KEYS = [("k_spread_uv", "k_spread_fwd"), ("k_spread_mma", "k_spread_fwd"), ("k_bwd_gather", "k_bwd_gather"),
+KEYS = [("k_spread_f8", "k_spread_fwd"), ("k_spread_uv", "k_spread_fwd"), ("k_dgemm_tn_tma", "k_dgemm_tn"),
+        ("k_dgemm_tn", "k_dgemm_tn"), ("k_spread_mma", "k_spread_fwd"), ("k_bwd_gather", "k_bwd_gather"),
         ("k_col_scatter", "k_col_scatter"), ("k_z_sort", "k_z_sort"), ("k_tile_hist", "k_tile_hist"),
         ("k_col_scan", "k_col_scan"), ("k_tile_sort", "k_tile_sort"), ("k_z_tiles", "k_z_tiles"),
         ("k_core_sum", "k_core_sum")]
@@ -21,6 +22,7 @@ M = {"time_us": "gpu__time_duration.sum", "dram_read": "dram__bytes_read.sum",
      "dram_write": "dram__bytes_write.sum", "inst": "smsp__inst_executed.sum",
      "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
      "dmma_pct": "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+     "dmma_inst": "sm__inst_executed_pipe_tensor_subpipe_dmma.sum",
      "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
      "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
      "l1tex_pct": "l1tex__throughput.avg.pct_of_peak_sustained_active",

@@ -210,11 +210,15 @@ __global__ void __launch_bounds__(THREADS) k_dgemm_tn_tma(int64_t M, int64_t N, 
     double* As = reinterpret_cast<double*>(base);                       // [S][BK][BM]
     double* Bs = reinterpret_cast<double*>(base + TSTAGES * kTmaA);     // [S][BN][BK] swizzled
     uint64_t* full = reinterpret_cast<uint64_t*>(base + TSTAGES * (kTmaA + kTmaB));
-    out += blockIdx.z * sout;
-    const int za = zA ? (int)blockIdx.z : 0, zb = zB ? (int)blockIdx.z : 0;
+    // grid (batch, m tile, n tile): the batch entries sharing an operand tile
+    // (the broadcast mesh of the per-term passes) are scheduled together, so
+    // the tile is read from DRAM once and served from L2 to the rest
+    const int bz = blockIdx.x;
+    out += bz * sout;
+    const int za = zA ? bz : 0, zb = zB ? bz : 0;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 1, wn = warp & 1;
-    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.z * BN;
     const int ktiles = (int)((K + BK - 1) / BK);
     if (tid == 0) {
         for (int s = 0; s < TSTAGES; ++s) mbarrier_init(full + s, 1);
@@ -405,7 +409,7 @@ void dgemm_tn_batched(cudaStream_t s, int64_t M, int64_t N, int64_t K, const dou
     }();
     const bool tma_ok = tma_env && (M % 2 == 0) && (K % 2 == 0) && ((uintptr_t)in % 16 == 0) &&
                         ((uintptr_t)F % 16 == 0) && (sin % 2 == 0) && (sF % 2 == 0) &&
-                        M < (int64_t(1) << 31) && N < (int64_t(1) << 31) && K < (int64_t(1) << 31);
+                        K < (int64_t(1) << 31) && grid.x <= 65535 && grid.y <= 65535;
     if (tma_ok) {
         CUtensorMap ta, tb;
         if (make_map(&ta, in, K, M, sin, batch, BM, BK, false) &&
@@ -415,7 +419,8 @@ void dgemm_tn_batched(cudaStream_t s, int64_t M, int64_t N, int64_t K, const dou
                 KB_CUDA(cudaFuncSetAttribute(k_dgemm_tn_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)kSmemTma));
             });
-            k_dgemm_tn_tma<<<grid, THREADS, kSmemTma, s>>>(M, N, K, ta, tb, sin ? 1 : 0, sF ? 1 : 0,
+            const dim3 tgrid((unsigned)batch, grid.x, grid.y);
+            k_dgemm_tn_tma<<<tgrid, THREADS, kSmemTma, s>>>(M, N, K, ta, tb, sin ? 1 : 0, sF ? 1 : 0,
                                                            out, accumulate ? 1 : 0, sout);
             KB_CHECK_LAUNCH();
             return;

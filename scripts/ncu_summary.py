@@ -45,7 +45,7 @@ for d in data:
         if k.startswith("dram_") and not k.endswith("pct"):
             v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         if k == "time_us":
-            v *= {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(u, 1)
+            v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3}.get(u, 1)
         e[k] = v
     e["dram_bytes"] = e.get("dram_read", 0) + e.get("dram_write", 0)
     st = [(h[i], float(d[i] or 0)) for i in range(len(h))

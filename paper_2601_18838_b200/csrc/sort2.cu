@@ -376,12 +376,11 @@ __host__ inline int whole_cap_for(int K2) {
 
 // Steps 2-5 of the whole-column sort: the column's m records and indices are
 // staged in shared memory in ascending particle order and cnt is zeroed.
-template <int ZB>
-__device__ __forceinline__ void z_whole_body(const Geometry& g, int col, int cs, int m, int64_t n,
-                                             const double4* s_rec, const int32_t* s_idx,
-                                             uint16_t* s_inv, uint8_t* s_z, uint16_t* cnt,
-                                             int32_t* __restrict__ perm, int32_t* __restrict__ start,
-                                             double4* __restrict__ sp, int32_t* wsum) {
+template <int ZB, class ZOf, class Emit>
+__device__ __forceinline__ void z_whole_core(const Geometry& g, int col, int cs, int m, int64_t n,
+                                             ZOf zof, Emit emit, uint16_t* s_inv, uint8_t* s_z,
+                                             uint16_t* cnt, int32_t* __restrict__ start,
+                                             int32_t* wsum) {
     const int K2 = g.K[2], ncol = g.K[0] * g.K[1];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 #ifdef ZSORT_PROFILE
@@ -401,7 +400,7 @@ __device__ __forceinline__ void z_whole_body(const Geometry& g, int col, int cs,
     const int lo = min(m, tid * per), hi = min(m, lo + per);
     unsigned long long n0 = 0, n1 = 0, n2 = 0, n3 = 0;
     for (int j = lo; j < hi; ++j) {
-        const int z = rec_c2(g, s_rec[j]);
+        const int z = zof(j);
         s_z[j] = (uint8_t)z;
         const unsigned long long inc = 1ull << ((z & 15) * 4);
         const int wq = z >> 4;
@@ -462,11 +461,7 @@ __device__ __forceinline__ void z_whole_body(const Geometry& g, int col, int cs,
     __syncthreads();
     ZSTAMP();
     // 5: the column leaves in cell order as one contiguous run
-    for (int k = tid; k < m; k += kZThreads) {
-        const int j = s_inv[k];
-        perm[cs + k] = s_idx[j];
-        if (sp) st_rec(sp + cs + k, s_rec[j]);
-    }
+    emit(s_inv);
 #ifdef ZSORT_PROFILE
     __syncthreads();
     ZSTAMP();
@@ -475,6 +470,65 @@ __device__ __forceinline__ void z_whole_body(const Geometry& g, int col, int cs,
                (int)__smid(), m, T[1] - T[0], T[2] - T[1], T[3] - T[2], T[4] - T[3], T[5] - T[4], T[0]);
 #endif
 #undef ZSTAMP
+}
+
+// The record path: c2 recomputed from the staged record, records written out.
+template <int ZB>
+__device__ __forceinline__ void z_whole_body(const Geometry& g, int col, int cs, int m, int64_t n,
+                                             const double4* s_rec, const int32_t* s_idx,
+                                             uint16_t* s_inv, uint8_t* s_z, uint16_t* cnt,
+                                             int32_t* __restrict__ perm, int32_t* __restrict__ start,
+                                             double4* __restrict__ sp, int32_t* wsum) {
+    z_whole_core<ZB>(
+        g, col, cs, m, n, [&](int j) { return rec_c2(g, s_rec[j]); },
+        [&](const uint16_t* inv) {
+            for (int k = threadIdx.x; k < m; k += kZThreads) {
+                const int j = inv[k];
+                perm[cs + k] = s_idx[j];
+                if (sp) st_rec(sp + cs + k, s_rec[j]);
+            }
+        },
+        s_inv, s_z, cnt, start, wsum);
+}
+
+// The key path (k_z_tiles_ko): staged (particle, c2) pairs; the records are
+// gathered from the input arrays (L2-resident after the tile pass) straight
+// into their sorted place, four at a time per thread.
+template <int ZB>
+__device__ __forceinline__ void z_whole_pairs(const Geometry& g, int col, int cs, int m, int64_t n,
+                                              const int2* s_pair, uint16_t* s_inv, uint8_t* s_z,
+                                              uint16_t* cnt, int32_t* __restrict__ perm,
+                                              int32_t* __restrict__ start, const double* __restrict__ xyz,
+                                              const double* __restrict__ q, double4* __restrict__ sp,
+                                              int32_t* wsum) {
+    z_whole_core<ZB>(
+        g, col, cs, m, n, [&](int j) { return s_pair[j].y; },
+        [&](const uint16_t* inv) {
+            for (int k0 = threadIdx.x; k0 < m; k0 += 4 * kZThreads) {
+                int id[4];
+                double4 r[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = k0 + u * kZThreads;
+                    id[u] = k < m ? s_pair[inv[k]].x : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (sp && id[u] >= 0) {
+                        const int64_t i = id[u];
+                        r[u] = make_double4(__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1),
+                                            __ldg(xyz + 3 * i + 2), __ldg(q + i));
+                    }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (id[u] >= 0) {
+                        const int k = k0 + u * kZThreads;
+                        perm[cs + k] = id[u];
+                        if (sp) st_rec(sp + cs + k, r[u]);
+                    }
+            }
+        },
+        s_inv, s_z, cnt, start, wsum);
 }
 
 template <int ZB>
@@ -535,6 +589,32 @@ struct ContiguousSrc {
     int cs;
     __device__ int64_t operator()(int j) const { return (int64_t)cs + j; }
 };
+// Element access of the chunked column sort: records (rec2, idx2) or the key
+// path's (particle, c2) pairs with the records gathered from the inputs.
+struct RecAcc {
+    const Geometry* g;
+    const int32_t* idx2;
+    const double4* rec2;
+    __device__ int z(int64_t sj) const { return rec_c2(*g, ld_rec(rec2 + sj)); }
+    __device__ int idx(int64_t sj) const { return __ldg(idx2 + sj); }
+    __device__ double4 rec(int64_t sj, int) const { return ld_rec(rec2 + sj); }
+};
+struct PairAcc {
+    const int2* pairs;
+    const double* xyz;
+    const double* q;
+    __device__ int z(int64_t sj) const { return __ldg(&pairs[sj].y); }
+    __device__ int idx(int64_t sj) const { return __ldg(&pairs[sj].x); }
+    __device__ double4 rec(int64_t, int i) const {
+        return make_double4(__ldg(xyz + 3 * (int64_t)i), __ldg(xyz + 3 * (int64_t)i + 1),
+                            __ldg(xyz + 3 * (int64_t)i + 2), q ? __ldg(q + i) : 0.0);
+    }
+};
+template <int ZB, class Src, class Acc>
+__device__ __forceinline__ void z_sort_chunked_acc(const Geometry& g, int col, int cs, int m, Src src,
+                                                   Acc acc, int64_t n, int32_t* __restrict__ perm,
+                                                   int32_t* __restrict__ start,
+                                                   double4* __restrict__ sp, unsigned char* zsm);
 template <int ZB, class Src>
 __device__ __forceinline__ void z_sort_chunked(const Geometry& g, int col, int cs, int m, Src src,
                                                int64_t n, const int32_t* __restrict__ idx2,
@@ -542,6 +622,13 @@ __device__ __forceinline__ void z_sort_chunked(const Geometry& g, int col, int c
                                                int32_t* __restrict__ perm,
                                                int32_t* __restrict__ start,
                                                double4* __restrict__ sp, unsigned char* zsm) {
+    z_sort_chunked_acc<ZB>(g, col, cs, m, src, RecAcc{&g, idx2, rec2}, n, perm, start, sp, zsm);
+}
+template <int ZB, class Src, class Acc>
+__device__ __forceinline__ void z_sort_chunked_acc(const Geometry& g, int col, int cs, int m, Src src,
+                                                   Acc acc, int64_t n, int32_t* __restrict__ perm,
+                                                   int32_t* __restrict__ start,
+                                                   double4* __restrict__ sp, unsigned char* zsm) {
     const int K2 = g.K[2], ncol = g.K[0] * g.K[1];
     const ZLayout L(K2);
     double4* s_rec = reinterpret_cast<double4*>(zsm + L.rec);
@@ -554,7 +641,7 @@ __device__ __forceinline__ void z_sort_chunked(const Geometry& g, int col, int c
     for (int e = tid; e < K2; e += kZThreads) zrun[e] = 0;
     __syncthreads();
     // column histogram over c2 (order-free)
-    for (int j = tid; j < m; j += kZThreads) atomicAdd(&zrun[rec_c2(g, ld_rec(rec2 + src(j)))], 1);
+    for (int j = tid; j < m; j += kZThreads) atomicAdd(&zrun[acc.z(src(j))], 1);
     __syncthreads();
     if (w == 0) {  // cell starts; zrun becomes each cell's running output position
         int carry = cs;
@@ -585,9 +672,9 @@ __device__ __forceinline__ void z_sort_chunked(const Geometry& g, int col, int c
             zr[u] = -1 - lane;
             if (jl < cm) {
                 const int64_t sj = src(c0 + jl);
-                v[u] = ld_rec(rec2 + sj);
-                ir[u] = __ldg(idx2 + sj);
-                zr[u] = rec_c2(g, v[u]);
+                ir[u] = acc.idx(sj);
+                zr[u] = acc.z(sj);
+                if (sp) v[u] = acc.rec(sj, ir[u]);
             }
         }
         __syncthreads();
@@ -639,7 +726,7 @@ __device__ __forceinline__ void z_sort_chunked(const Geometry& g, int col, int c
                 const int lp = base + __popc(peers & ((1u << lane) - 1));
                 s_idx[lp] = ir[u];
                 s_z[lp] = (uint16_t)zr[u];
-                s_rec[lp] = v[u];
+                if (sp) s_rec[lp] = v[u];
             }
             __syncwarp();
             if (act && lane == __ffs(peers) - 1) cnt[zr[u] * kZWarps + w] = base + __popc(peers);
@@ -963,6 +1050,255 @@ __global__ void __launch_bounds__(kZThreads, 2) k_z_tiles(Geometry g, int64_t n,
                                      wsum);
 }
 
+// ---- key path: the tile pass moves (particle, c2) pairs, not records ----------
+// k_tile_keys   the tile pass of k_tile_sort reading only x, y, z (24 B per
+//               particle) and writing 8-byte (particle, c2) pairs: the tile's
+//               shared-memory stage is a fifth of the record path's
+// k_z_tiles_ko  the column pass on pairs (one 8-byte cp.async per element);
+//               the sorted records are gathered from the input arrays, which
+//               the tile pass has just brought into L2, straight into sp
+// The order, cell starts and records are identical to the record path.
+struct TileKeysLayout {
+    size_t pair, wc, tc, cb, total;
+    __host__ __device__ TileKeysLayout(int ncol, int tile) {
+        pair = 0;
+        wc = pair + sizeof(int2) * tile;
+        tc = wc + ((sizeof(uint16_t) * kTileWarps * ncol + 15) & ~size_t(15));
+        cb = tc + sizeof(int32_t) * ncol;
+        total = cb + sizeof(int32_t) * (ncol + 1);
+    }
+};
+
+#ifndef KEYS_MINB
+#define KEYS_MINB 4  // 64 registers, four tiles per SM (config 3: sort stage 59.8 -> 55.4 us with ZKO_MINB 3)
+#endif
+#ifndef ZKO_MINB
+#define ZKO_MINB 3
+#endif
+template <int CB, int TR>
+__global__ void __launch_bounds__(kTileWarps * 32, KEYS_MINB) k_tile_keys(Geometry g, int64_t n,
+                                                               const double* __restrict__ xyz,
+                                                               int32_t* __restrict__ toff,
+                                                               int2* __restrict__ pairs,
+                                                               unsigned long long* bad) {
+    extern __shared__ __align__(16) unsigned char tsm[];
+    __shared__ int32_t wsum[32];
+    const int ncol = g.K[0] * g.K[1];
+    constexpr int kTT = TR * 32 * kTileWarps;
+    const TileKeysLayout TL(ncol, kTT);
+    int2* s_pair = reinterpret_cast<int2*>(tsm + TL.pair);
+    uint16_t* wc = reinterpret_cast<uint16_t*>(tsm + TL.wc);  // [kTileWarps][ncol]
+    int32_t* tc = reinterpret_cast<int32_t*>(tsm + TL.tc);
+    int32_t* cb = reinterpret_cast<int32_t*>(tsm + TL.cb);
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    for (int e = tid; e < (int)((TL.tc - TL.wc) / 16); e += blockDim.x)
+        reinterpret_cast<uint4*>(wc)[e] = make_uint4(0u, 0u, 0u, 0u);
+    const int64_t tbase = (int64_t)blockIdx.x * kTT;
+    const int64_t wbase = tbase + w * (TR * 32);
+    double px[TR], py[TR], pz[TR];
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {  // every load of the warp's slice in flight
+        const int64_t i = wbase + r * 32 + lane;
+        if (i < n) {
+            px[r] = __ldg(xyz + 3 * i);
+            py[r] = __ldg(xyz + 3 * i + 1);
+            pz[r] = __ldg(xyz + 3 * i + 2);
+        }
+    }
+    const double b = __dmul_rn(2.0, g.radius), y = g.inv_diam;
+    int colr[TR], c2r[TR];
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+        const int64_t i = wbase + r * 32 + lane;
+        colr[r] = -1;
+        c2r[r] = 0;
+        if (i < n) {
+            const double p0 = px[r], p1 = py[r], p2 = pz[r];
+            if (fabs(p0 - g.center[0]) > g.radius || fabs(p1 - g.center[1]) > g.radius ||
+                fabs(p2 - g.center[2]) > g.radius)
+                atomicMin(&bad[0], (unsigned long long)i);  // Box3::contains (geometry.hpp:36-40)
+            const int c0 = axis_cell2(p0, g.center[0], g.radius, g.K[0], b, y);
+            const int c1 = axis_cell2(p1, g.center[1], g.radius, g.K[1], b, y);
+            const int c2 = axis_cell2(p2, g.center[2], g.radius, g.K[2], b, y);
+            if (c0 < g.x_lo || c0 >= g.x_hi || c1 < g.y_lo || c1 >= g.y_hi || c2 < g.z_lo || c2 >= g.z_hi)
+                atomicOr(&bad[1], 2ull);  // not in this plan's cell block
+            colr[r] = c0 * g.K[1] + c1;
+            c2r[r] = c2;
+        }
+    }
+    __syncthreads();
+    unsigned pk[TR];
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+        const bool act = colr[r] >= 0;
+        const int col = act ? colr[r] : -1 - lane;
+        const unsigned peers = warp_peers<CB>(col);
+        pk[r] = peers;
+        if (act && lane == __ffs(peers) - 1) wc[w * ncol + col] += (uint16_t)__popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int c = tid; c < ncol; c += blockDim.x) {
+        int run = 0;
+#pragma unroll
+        for (int k = 0; k < kTileWarps; ++k) {
+            const int t = wc[k * ncol + c];
+            wc[k * ncol + c] = (uint16_t)run;
+            run += t;
+        }
+        tc[c] = run;
+    }
+    __syncthreads();
+    block_col_bases(tc, ncol, cb, wsum);
+    int32_t* trow = toff + (int64_t)blockIdx.x * (ncol + 1);
+    for (int c = tid; c <= ncol; c += blockDim.x) trow[c] = cb[c];
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+        const bool act = colr[r] >= 0;
+        const unsigned peers = pk[r];
+        int base = 0;
+        if (act) base = cb[colr[r]] + wc[w * ncol + colr[r]];
+        __syncwarp();
+        if (act) {
+            if (lane == __ffs(peers) - 1) wc[w * ncol + colr[r]] += (uint16_t)__popc(peers);
+            const int pos = base + __popc(peers & ((1u << lane) - 1));
+            s_pair[pos] = make_int2((int32_t)(wbase + r * 32 + lane), c2r[r]);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    const int tn = cb[ncol];
+    for (int k = tid; k < tn; k += blockDim.x) pairs[tbase + k] = s_pair[k];
+}
+
+__device__ __forceinline__ void cp_async8_s(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Whole-column layout of the key path: pairs, inverse order, c2, counters.
+struct ZPairsLayout {
+    size_t pair, inv, z, cnt, total;
+    __host__ __device__ ZPairsLayout(int K2, int cap) {
+        pair = 0;
+        inv = sizeof(int2) * cap;
+        z = inv + sizeof(uint16_t) * cap;
+        cnt = z + sizeof(uint8_t) * cap;
+        cnt = (cnt + 15) & ~size_t(15);
+        total = cnt + sizeof(uint16_t) * (size_t)K2 * kZThreads;
+    }
+};
+// 4-bit per-thread counters: at most 15 of a thread's slice in one cell
+constexpr int kZPairsCap = 15 * kZThreads;
+__host__ inline int pairs_cap_for(int K2) {
+    if (K2 > 64) return 0;
+    for (int cap = kZPairsCap; cap >= 1024; cap -= 256)
+        if (ZPairsLayout(K2, cap).total <= kZWholeMaxSmem) return cap;
+    return 0;
+}
+
+template <int ZB>
+__global__ void __launch_bounds__(kZThreads, ZKO_MINB) k_z_tiles_ko(Geometry g, int64_t n, int ntiles, int tile,
+                                                           int whole_cap,
+                                                           const int32_t* __restrict__ toff,
+                                                           const int2* __restrict__ pairs,
+                                                           const double* __restrict__ xyz,
+                                                           const double* __restrict__ q,
+                                                           int32_t* __restrict__ perm,
+                                                           int32_t* __restrict__ start,
+                                                           double4* __restrict__ sp) {
+    extern __shared__ __align__(16) unsigned char zsm[];
+    __shared__ int32_t wsum[32];
+    const int col = blockIdx.x, ncol = g.K[0] * g.K[1], K2 = g.K[2];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int per = (ntiles + kZThreads - 1) / kZThreads;
+    const int lo = min(ntiles, tid * per), hi = min(ntiles, lo + per);
+    int a_[4], e_[4];
+    int csum = 0, psum = 0;
+    if (per <= 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (lo + u < hi) {
+                a_[u] = __ldg(toff + (int64_t)(lo + u) * (ncol + 1) + col);
+                e_[u] = __ldg(toff + (int64_t)(lo + u) * (ncol + 1) + col + 1);
+            }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (lo + u < hi) {
+                csum += a_[u];
+                psum += e_[u] - a_[u];
+            }
+    } else {
+        for (int t = lo; t < hi; ++t) {
+            const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
+            csum += a;
+            psum += __ldg(toff + (int64_t)t * (ncol + 1) + col + 1) - a;
+        }
+    }
+    int x = psum, cx = csum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y1 = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y1;
+        cx += __shfl_xor_sync(0xffffffffu, cx, o);
+    }
+    if (lane == 31) wsum[w] = x;
+    if (lane == 0) wsum[16 + w] = cx;
+    __syncthreads();
+    int off = 0, cs = 0;
+    for (int k = 0; k < kZWarps; ++k) {
+        off += k < w ? wsum[k] : 0;
+        cs += wsum[16 + k];
+    }
+    int m = 0;
+    for (int k = 0; k < kZWarps; ++k) m += wsum[k];
+    const bool whole = ZB <= 6 && m <= whole_cap;  // uniform per CTA
+    int run = off + x - psum;
+    if (!whole) {  // piece tables, binary-searched per element (chunked column sort)
+        const ZTilesLayout TLc(K2, ntiles, 0);
+        int32_t* pre = reinterpret_cast<int32_t*>(zsm + TLc.tables);
+        int32_t* srca = pre + ntiles + 1;
+        for (int t = lo; t < hi; ++t) {
+            const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
+            srca[t] = t * tile + a;
+            pre[t] = run;
+            run += __ldg(toff + (int64_t)t * (ncol + 1) + col + 1) - a;
+        }
+        if (tid == 0) pre[ntiles] = m;
+        __syncthreads();
+        z_sort_chunked_acc<ZB>(g, col, cs, m, PieceSrc{pre, srca, ntiles}, PairAcc{pairs, xyz, q}, n, perm,
+                               start, sp, zsm);
+        return;
+    }
+    const ZPairsLayout L(K2, whole_cap);
+    int2* s_pair = reinterpret_cast<int2*>(zsm + L.pair);
+    uint16_t* s_inv = reinterpret_cast<uint16_t*>(zsm + L.inv);
+    uint8_t* s_z = reinterpret_cast<uint8_t*>(zsm + L.z);
+    uint16_t* cnt = reinterpret_cast<uint16_t*>(zsm + L.cnt);
+    // every thread copies its own pieces, in tile order (ascending particles)
+    if (per <= 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (lo + u < hi) {
+                const int c = e_[u] - a_[u];
+                const int64_t src0 = (int64_t)(lo + u) * tile + a_[u];
+                for (int k = 0; k < c; ++k) cp_async8_s(s_pair + run + k, pairs + src0 + k);
+                run += c;
+            }
+    } else {
+        for (int t = lo; t < hi; ++t) {
+            const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
+            const int c = __ldg(toff + (int64_t)t * (ncol + 1) + col + 1) - a;
+            const int64_t src0 = (int64_t)t * tile + a;
+            for (int k = 0; k < c; ++k) cp_async8_s(s_pair + run + k, pairs + src0 + k);
+            run += c;
+        }
+    }
+    for (int e = tid; e < K2 * kZThreads; e += kZThreads) cnt[e] = 0;
+    cp_async_wait_all();
+    __syncthreads();
+    z_whole_pairs<(ZB <= 6 ? ZB : 6)>(g, col, cs, m, n, s_pair, s_inv, s_z, cnt, perm, start, xyz, q, sp,
+                                      wsum);
+}
+
 // Instantiation for an even key width in [2, 16].
 template <class F>
 auto pick_bits(int b, F f) {
@@ -1020,7 +1356,11 @@ static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, 
     // Tile rounds: the fewest (waves x tile length) at two CTAs per SM, among
     // tiles holding >= 4 particles per column on average (the pieces k_z_tiles
     // gathers); ties go to the longer tile. Config 3: 559 tiles of 1792.
-    const int slots = 2 * sm_count();
+    static const bool keys_on = [] {
+        const char* e = getenv("KPME_SORT_KEYS");
+        return !(e && *e == '0');
+    }();
+    const int slots = (keys_on && (q || !sp) ? KEYS_MINB : 2) * sm_count();
     int tr = 8;
     {
         int64_t best = -1;
@@ -1056,11 +1396,55 @@ static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, 
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
         }
     });
+    int l = 0;
+    // Key path (default): the tile pass moves 8-byte (particle, c2) pairs and
+    // the column pass gathers the records from the inputs. KPME_SORT_KEYS=0:
+    // the record path.
+    static const bool keys_env = [] {
+        const char* e = getenv("KPME_SORT_KEYS");
+        return !(e && *e == '0');
+    }();
+    const int pcap = pairs_cap_for(g.K[2]);
+    const TileKeysLayout TK(ncol, tile);
+    const ZTilesLayout ZLc(g.K[2], ntiles, 0);
+    const size_t kzsmem = std::max(ZLc.total_chunked, pcap ? ZPairsLayout(g.K[2], pcap).total : 0);
+    if (keys_env && (q || !sp) && TK.total <= kTileMaxSmem && kzsmem <= 160 * 1024) {
+        static PerDevice keys_once;
+        once_per_device(keys_once, [&] {
+            for (int bb = 2; bb <= 16; bb += 2) {
+                for (int r : {4, 7, 8})
+                    KB_CUDA(cudaFuncSetAttribute(pick_bits(bb, [r](auto B) {
+                                                     return pick_rounds(r, [](auto T) {
+                                                         return &k_tile_keys<decltype(B)::value, decltype(T)::value>;
+                                                     });
+                                                 }),
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileMaxSmem));
+                KB_CUDA(cudaFuncSetAttribute(pick_bits(bb, [](auto B) { return &k_z_tiles_ko<decltype(B)::value>; }),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+            }
+        });
+        int2* pairs = reinterpret_cast<int2*>(b.rec);
+        if (n > 0) {
+            auto tk = pick_bits(cb, [tr](auto B) {
+                return pick_rounds(tr, [](auto T) { return &k_tile_keys<decltype(B)::value, decltype(T)::value>; });
+            });
+            tk<<<ntiles, kTileWarps * 32, TK.total, s>>>(g, n, xyz, b.hist, pairs, b.bad);
+            KB_CHECK_LAUNCH();
+            ++l;
+        } else {
+            KB_CUDA(cudaMemsetAsync(b.hist, 0, sizeof(int32_t) * (ncol + 1), s));
+        }
+        auto zk = pick_bits(zb, [](auto B) { return &k_z_tiles_ko<decltype(B)::value>; });
+        zk<<<ncol, kZThreads, kzsmem, s>>>(g, n, ntiles, tile, pcap, b.hist, pairs, xyz, q, b.perm, b.start,
+                                           sp);
+        KB_CHECK_LAUNCH();
+        if (launches) *launches += l + 1;
+        return true;
+    }
     auto tile_kernel = pick_bits(cb, [tr](auto B) {
         return pick_rounds(tr, [](auto T) { return &k_tile_sort<decltype(B)::value, decltype(T)::value>; });
     });
     auto z_kernel = pick_bits(zb, [](auto B) { return &k_z_tiles<decltype(B)::value>; });
-    int l = 0;
     if (n > 0) {
         tile_kernel<<<ntiles, kTileWarps * 32, TL.total, s>>>(g, n, xyz, q, b.hist, b.idx2, b.rec, b.bad);
         KB_CHECK_LAUNCH();

@@ -211,10 +211,9 @@ void setup(DS* d) {
         r.bounds = r.alloc<int>(b.size());
         KB_CUDA(cudaMemcpy(r.bounds, b.data(), sizeof(int) * b.size(), cudaMemcpyHostToDevice));
         const int nz = d->zhi[r.rank] - d->zlo[r.rank];
-        const int mine = (d->nt - r.rank + W - 1) / W;  // rank_split terms
+        // rank_split applies its terms one kron_local call each (strided operands)
         r.ws_bytes = std::max(kb::kron_local_workspace_bytes(d->n0, d->n1, nz, d->n2, d->nt),
-                              kb::kron_local_workspace_bytes(d->n0, d->n1, d->n2, d->n2,
-                                                             std::max(1, mine)));
+                              kb::kron_local_workspace_bytes(d->n0, d->n1, d->n2, d->n2, 1));
         r.ws = r.alloc<double>(r.ws_bytes / sizeof(double) + 1);
         r.ypart = r.alloc<double>(mesh);
         r.ysm = r.alloc<double>((size_t)W * d->blk());

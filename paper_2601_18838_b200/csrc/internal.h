@@ -184,10 +184,19 @@ struct ColumnArgs {
     // monomial gather: a thread takes two adjacent particles (pays off when
     // cells are full enough that a warp's pairs rarely straddle a cell)
     int gpairs;
+    // direct records (hot path): the sort writes no sorted copy of the
+    // particles; the spread and gather read record s as
+    // (xyz[perm[s]], qv[perm[s]]) from the inputs, L2-resident after the sort
+    int direct;
+    const double* xyz;
+    const double* qv;
 };
 enum SpreadMode { SPREAD_PARTICLES = 0, SPREAD_FROM_CELLS = 1 };
 enum GatherMode { GATHER_FROM_B2 = 0, GATHER_FROM_CELLS = 1, PSI_ONLY = 2 };
 void launch_spread_fwd(const ColumnArgs& a, int mode, bool want_fwd, cudaStream_t s);
+// The kernels that read records through ColumnArgs::direct (the split-exponent
+// spread and the monomial gather) serve this geometry.
+bool direct_records_ok(const Geometry& g);
 void launch_bwd_gather(const ColumnArgs& a, int mode, cudaStream_t s);
 
 // ---- core.cu ----------------------------------------------------------------

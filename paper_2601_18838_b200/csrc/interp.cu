@@ -996,6 +996,10 @@ __device__ __forceinline__ void cp_async16_sm(void* dst, const void* src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async8_sm(void* dst, const void* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -1134,14 +1138,30 @@ __global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_
     };
     norm();
     int pslot = 0, cslot = 0;
+    // direct records: the particle index of the chunk to be issued is loaded
+    // one chunk earlier (pidx), so the copies never wait on the perm load
+    int pidx = 0;
+    auto perm_at = [&]() {
+        return nc2 < zw1 ? __ldg(a.perm + min(nbase + lane, cell_hi_p(nc2) - 1)) : 0;
+    };
+    if (a.direct) pidx = perm_at();
     auto issue = [&]() {
         if (nc2 < zw1) {
-            const double4* src = a.sp + min(nbase + lane, cell_hi_p(nc2) - 1);
             double4* dst = ring + pslot * 32 + lane;
-            cp_async16_sm(dst, src);
-            cp_async16_sm(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(src) + 16);
+            if (a.direct) {
+                const double* src = a.xyz + 3 * (int64_t)pidx;
+                cp_async8_sm(dst, src);
+                cp_async8_sm(reinterpret_cast<char*>(dst) + 8, src + 1);
+                cp_async8_sm(reinterpret_cast<char*>(dst) + 16, src + 2);
+                cp_async8_sm(reinterpret_cast<char*>(dst) + 24, a.qv + pidx);
+            } else {
+                const double4* src = a.sp + min(nbase + lane, cell_hi_p(nc2) - 1);
+                cp_async16_sm(dst, src);
+                cp_async16_sm(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(src) + 16);
+            }
             nbase += 32;
             norm();
+            if (a.direct) pidx = perm_at();
         }
         cp_async_commit();
         pslot = pslot + 1 == M::RING ? 0 : pslot + 1;
@@ -1277,6 +1297,39 @@ __global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_
     if (lane == 0 && badw) atomicOr(&a.bad[1], 1ull);
     spread_epilogue<L, NW>(a, cr, sm, per_warp, t1off, RP, epi, red, qsum, want_fwd);
 }
+
+// Records s, s + stride, ... of the sorted order for one gather thread: the
+// record one step ahead and its particle index two steps ahead (with direct
+// records the record load needs the index; the gather needs no charge).
+struct RecStream {
+    const ColumnArgs* a;
+    int s1, stride;
+    double4 nr;
+    int ni, nni;
+    __device__ double4 fetch(int s, int i) const {
+        if (s >= s1) return make_double4(0.0, 0.0, 0.0, 0.0);
+        if (a->direct) {
+            const double* x = a->xyz + 3 * (int64_t)i;
+            return make_double4(__ldg(x), __ldg(x + 1), __ldg(x + 2), 0.0);
+        }
+        return ld_rec(a->sp + s);
+    }
+    __device__ int index(int s) const { return s < s1 ? __ldg(a->perm + s) : 0; }
+    __device__ void init(int s) {
+        ni = index(s);
+        nni = index(s + stride);
+        nr = fetch(s, ni);
+    }
+    // record and particle index of s (the stream's next element)
+    __device__ double4 next(int s, int& idx) {
+        const double4 r = nr;
+        idx = ni;
+        nr = fetch(s + stride, nni);
+        ni = nni;
+        nni = index(s + 2 * stride);
+        return r;
+    }
+};
 
 // Backward z-expansion + gather with compile-time L: psi for a batch of the
 // column's cells in shared memory, then one thread per particle,
@@ -1451,15 +1504,11 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
             const int s0 = gcst[0], s1 = gcst[nb];
             int cc = 0;
             double tmax = 0.0;
-            double4 pn = s0 + tid < s1 ? ld_rec(a.sp + s0 + tid) : make_double4(0.0, 0.0, 0.0, 0.0);
-            int dn = s0 + tid < s1 ? a.perm[s0 + tid] : 0;
+            RecStream rs{&a, s1, GT};
+            rs.init(s0 + tid);
             for (int s = s0 + tid; s < s1; s += GT) {
-                const double4 p = pn;  // software prefetch of the next particle
-                const int dst = dn;
-                if (s + GT < s1) {
-                    pn = ld_rec(a.sp + s + GT);
-                    dn = a.perm[s + GT];
-                }
+                int dst;
+                const double4 p = rs.next(s, dst);  // software prefetch of the next particle
                 while (gcst[cc + 1] <= s) ++cc;
                 const double* ps = psi + cc * L3;
                 const double4 x2 = gax[cc];  // (lo, hi, mid, inv)
@@ -1507,13 +1556,10 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
             const int s0 = gcst[0], s1 = gcst[nb];
             int cc = 0;
             double tmax = 0.0;
-            auto rec = [&](int s) {
-                return s < s1 ? ld_rec(a.sp + s) : make_double4(0.0, 0.0, 0.0, 0.0);
-            };
-            auto idx = [&](int s) { return s < s1 ? a.perm[s] : 0; };
             int sb = s0 + 2 * tid;
-            double4 pa = rec(sb), pb = rec(sb + 1);
-            int da = idx(sb), db = idx(sb + 1);
+            RecStream ra{&a, s1, 2 * GT}, rb{&a, s1, 2 * GT};
+            ra.init(sb);
+            rb.init(sb + 1);
             // nested Horner over the monomial coefficients C[a][b][c] of a cell:
             // z = sum_a t0^a sum_b t1^b sum_c t2^c C[a][b][c]
             auto horner1 = [&](const double* ps, const double (&t)[3]) {
@@ -1535,14 +1581,8 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
             };
             // warp-uniform trip count (lane 0 holds the warp's lowest pair)
             for (int wb = s0 + 64 * (tid >> 5); wb < s1; wb += 2 * GT, sb += 2 * GT) {
-                const double4 p0 = pa, p1 = pb;  // software prefetch of the next pair
-                const int d0 = da, d1 = db;
-                if (sb + 2 * GT < s1) {
-                    pa = rec(sb + 2 * GT);
-                    pb = rec(sb + 2 * GT + 1);
-                    da = idx(sb + 2 * GT);
-                    db = idx(sb + 2 * GT + 1);
-                }
+                int d0, d1;
+                const double4 p0 = ra.next(sb, d0), p1 = rb.next(sb + 1, d1);  // prefetched pair
                 const bool has0 = sb < s1, has1 = sb + 1 < s1;
                 while (gcst[cc + 1] <= min(sb, s1 - 1)) ++cc;
                 int cc1 = cc;
@@ -1596,15 +1636,11 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
                 atomicOr(&a.bad[1], 1ull);
         } else if (MODE != PSI_ONLY && !(GATHER_SKIP & 1)) {
             const int s0 = a.start[cell0], s1 = a.start[cell0 + (cb1 - cb0)];
-            double4 pn = s0 + tid < s1 ? ld_rec(a.sp + s0 + tid) : make_double4(0.0, 0.0, 0.0, 0.0);
-            int dn = s0 + tid < s1 ? a.perm[s0 + tid] : 0;
+            RecStream rs{&a, s1, GT};
+            rs.init(s0 + tid);
             for (int s = s0 + tid; s < s1; s += GT) {
-                const double4 p = pn;  // software prefetch of the next particle
-                const int dst = dn;
-                if (s + GT < s1) {
-                    pn = ld_rec(a.sp + s + GT);
-                    dn = a.perm[s + GT];
-                }
+                int dst;
+                const double4 p = rs.next(s, dst);  // software prefetch of the next particle
                 const int c2 = axis_cell(p.z, g.center[2], g.radius, g.K[2], g.inv_diam);
                 const double* ps = psi + (c2 - cb0) * L3;
                 const CellAxis ax2 = cell_axis_tab(a.cellax[2], c2);
@@ -1716,6 +1752,9 @@ void launch_spread_mma_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
 #endif
 #ifndef SPREAD_F8
 #define SPREAD_F8 1  // split-exponent spread for L = 4, 6
+#endif
+#ifndef DIRECT_RECORDS
+#define DIRECT_RECORDS 1
 #endif
 template <int L>
 bool launch_spread_f8_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
@@ -1829,6 +1868,18 @@ void launch_gather_t(const ColumnArgs& a0, int mode, cudaStream_t s) {
 }
 
 }  // namespace
+
+bool direct_records_ok(const Geometry& g) {
+    if (!DIRECT_RECORDS || !SPREAD_F8 || g.R > 32) return false;
+    size_t smem;
+    if (g.L == 4)
+        smem = sizeof(double) * spread_f8_smem_doubles<4>(g.R, g.n[2]);
+    else if (g.L == 6)
+        smem = sizeof(double) * spread_f8_smem_doubles<6>(g.R, g.n[2]);
+    else
+        return false;
+    return smem <= 200 * 1024;
+}
 
 void launch_spread_fwd(const ColumnArgs& a, int mode, bool want_fwd, cudaStream_t s) {
     static PerDevice attr_once;

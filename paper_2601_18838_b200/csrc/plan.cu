@@ -116,12 +116,23 @@ int gather_pairs(const kb::Geometry& g, int64_t n) {
     return cells > 0 && n >= 64 * cells ? 1 : 0;
 }
 
-void sort_and_permute(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q) {
+void sort_and_permute(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q,
+                      bool records = true) {
     // the sort also writes the cell-ordered particle records when q is given
+    // (not for direct records: the kernels read them through perm)
+    double4* sp = q && records ? p->sp : nullptr;
     if (p->use_sort2)
-        kb::launch_sort2(p->g, n, xyz, p->sb, p->stream, &p->launches, q, q ? p->sp : nullptr);
+        kb::launch_sort2(p->g, n, xyz, p->sb, p->stream, &p->launches, q, sp);
     else
-        kb::launch_sort(p->g, n, xyz, p->sb, p->stream, &p->launches, q, q ? p->sp : nullptr);
+        kb::launch_sort(p->g, n, xyz, p->sb, p->stream, &p->launches, q, sp);
+}
+
+// Direct records on the collapsed hot path (split-exponent spread, monomial
+// gather): the kernels read record s as (xyz, q)[perm[s]].
+void set_direct(kpme_gpu_plan p, kb::ColumnArgs& a, const double* xyz, const double* q) {
+    a.direct = p->direct ? 1 : 0;
+    a.xyz = xyz;
+    a.qv = q;
 }
 
 // Hot path for L <= 8: factor rows in the monomial basis of each cell.
@@ -192,12 +203,14 @@ void pipeline(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q, do
     p->launches = 0;
     record(p, 0);
     reset_flags(p);
-    sort_and_permute(p, n, xyz, q);
+    const bool dense = p->form == KPME_GPU_FORM_DENSE;
+    sort_and_permute(p, n, xyz, q, dense || !p->direct);
     record(p, 1);
     kb::ColumnArgs a = column_args(p);
     a.out = out;
     a.gpairs = gather_pairs(p->g, n);
-    if (p->form == KPME_GPU_FORM_DENSE) {
+    if (!dense) set_direct(p, a, xyz, q);
+    if (dense) {
         a.phi_cells = p->cells;
         kb::launch_spread_fwd(a, kb::SPREAD_PARTICLES, false, p->stream);
         record(p, 2);
@@ -229,16 +242,20 @@ void forward_half(kpme_gpu_plan p, int64_t n, const double* xyz, const double* q
         invalid("kpme_gpu: slab plans use the collapsed formulation");
     p->launches = 0;
     reset_flags(p);
-    sort_and_permute(p, n, xyz, q);
+    sort_and_permute(p, n, xyz, q, !p->direct);
     kb::ColumnArgs a = column_args(p);
+    set_direct(p, a, xyz, q);
     forward_core(p, a, core);
     p->last_n = n;
+    p->last_xyz = xyz;
+    p->last_q = q;
 }
 
 void backward_half(kpme_gpu_plan p, const double* core, double* out) {
     kb::ColumnArgs a = column_args(p);
     a.out = out;
     a.gpairs = gather_pairs(p->g, p->last_n);
+    set_direct(p, a, p->last_xyz, p->last_q);
     backward_gather(p, a, core);
 }
 
@@ -372,6 +389,7 @@ void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double
         a.sp = p->sp + off;
         a.perm = sb.perm;
         a.bad = sb.bad;
+        set_direct(p, a, p->xyz_d + 3 * off, p->q_d + off);
         mono_tables(p, a);
         return a;
     };
@@ -381,12 +399,13 @@ void execute_chunked(kpme_gpu_plan p, int64_t n, const double* xyz, const double
         KB_CUDA(cudaStreamWaitEvent(p->stream, p->ev_in[c], 0));
         kb::SortBuffers sb;
         kb::ColumnArgs a = chunk_args(c, sb);
+        double4* csp = p->direct ? nullptr : p->sp + off;
         if (p->use_sort2)
             kb::launch_sort2(g, nc, p->xyz_d + 3 * off, sb, p->stream, &p->launches, p->q_d + off,
-                             p->sp + off);
+                             csp);
         else
             kb::launch_sort(g, nc, p->xyz_d + 3 * off, sb, p->stream, &p->launches, p->q_d + off,
-                            p->sp + off);
+                            csp);
         a.Fpart = p->cFpart + (size_t)c * nb;
         a.fstride = C * nb;
         tr.mark("sort chunk " + std::to_string(c), p->stream);
@@ -661,6 +680,18 @@ void create_plan(const kpme_gpu_config* cfg, int64_t max_particles, const int lo
             p->sb.rank = p->alloc<int32_t>(p->cap);
             p->sb.rec = p->alloc<double4>(p->cap);
             p->use_sort2 = kb::sort2_supported(g);
+            {
+                // Off by default: the sort stage saves its record write-out
+                // (config 3: 55.8 -> 41.0 us) but the spread's scattered record
+                // reads cost nearly as much (45.9 -> 55.6 us) and the gather's
+                // 47.3 -> 50.4 us: -2 us at config 3, +28 us at config 4.
+                // KPME_DIRECT_RECORDS=1 turns it on (tested).
+                static const bool direct_env = [] {
+                    const char* e = getenv("KPME_DIRECT_RECORDS");
+                    return e && *e == '1';
+                }();
+                p->direct = direct_env && kb::direct_records_ok(g);
+            }
             if (p->use_sort2) {
                 const size_t E = kb::sort2_hist_entries(g, p->cap);
                 p->sb.hist = p->alloc<int32_t>(E);

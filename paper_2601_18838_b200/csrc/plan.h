@@ -31,7 +31,12 @@ struct kpme_gpu_plan_s {
     int form = KPME_GPU_FORM_COLLAPSED;
     int launches = 0;
     int64_t last_n = 0;
+    const double* last_xyz = nullptr;  // inputs of the last forward half (direct records)
+    const double* last_q = nullptr;
     bool use_sort2 = false;
+    // hot path reads particle records through perm from the inputs (no sorted
+    // copy written by the sort; ColumnArgs::direct)
+    bool direct = false;
 
     // factor tables
     double* tw = nullptr;

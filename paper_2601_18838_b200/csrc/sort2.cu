@@ -1435,6 +1435,9 @@ static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, 
             KB_CUDA(cudaMemsetAsync(b.hist, 0, sizeof(int32_t) * (ncol + 1), s));
         }
         auto zk = pick_bits(zb, [](auto B) { return &k_z_tiles_ko<decltype(B)::value>; });
+#ifdef ZKO_NOSP  // profiling ablation only: no record write-out (results invalid)
+        sp = nullptr;
+#endif
         zk<<<ncol, kZThreads, kzsmem, s>>>(g, n, ntiles, tile, pcap, b.hist, pairs, xyz, q, b.perm, b.start,
                                            sp);
         KB_CHECK_LAUNCH();

@@ -517,11 +517,13 @@ def test_e2e_clustered_cells(oracle, order):
     assert rel(z, oracle.kpme_apply(pb)) <= E2E_TOL
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "1k"])
+@pytest.mark.parametrize("variant", ["0", "1", "1k", "1kd"])
 def test_sort_variants_forced(variant):
     """The cell-sort variants of sort2.cu -- column scatter ("0"), tile sort
-    on records ("1", KPME_SORT_KEYS=0) and the default tile sort on
-    (particle, c2) pairs ("1k") -- forced for every shape where they fit:
+    on records ("1", KPME_SORT_KEYS=0), the default tile sort on
+    (particle, c2) pairs ("1k"), and the same with direct records ("1kd":
+    no sorted copy, the spread and gather read (xyz, q)[perm[s]]) -- forced
+    for every shape where they fit:
     the bit-exact sort tests, the clustered columns above the whole-column
     capacity (the chunked piece gather) and end to end at configs 2 and 3.
     The variant is read once per process, hence the subprocess."""
@@ -529,10 +531,12 @@ def test_sort_variants_forced(variant):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, KPME_SORT_TILES=variant[0], KPME_SORT_KEYS="1" if variant == "1k" else "0")
+    env = dict(os.environ, KPME_SORT_TILES=variant[0],
+               KPME_SORT_KEYS="1" if variant.startswith("1k") else "0",
+               KPME_DIRECT_RECORDS="1" if variant == "1kd" else "0")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
                         "tests/test_gpu_parity.py", "-k",
-                        "(sort and not variants) or clustered or cfg2_vs or cfg3_vs or chunk"],
+                        "(sort and not variants) or clustered or cfg2_vs or cfg3_vs or chunk or orders or water"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout

@@ -214,6 +214,29 @@ def fp64_peak(torch, device):
     return 2.0 * n ** 3 / (best * 1e-3) / 1e12
 
 
+class L2Flush:
+    """L2 flush between timed steps: a 256 MiB write (the whole L2 becomes lines of
+    the flush buffer), then a read of a second 256 MiB buffer, so those lines are
+    written back and L2 ends holding clean lines of neither input. Without the read
+    the step's first kernels also pay the write-back of the flush's dirty lines."""
+
+    def __init__(self, torch, dev):
+        self.torch = torch
+        self.w = torch.empty(FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
+        self.r = torch.zeros(FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
+        self.read_back = os.environ.get("KPME_BENCH_FLUSH_READ", "1") != "0"
+
+    def zero_(self):
+        self.w.zero_()
+        if self.read_back:
+            self.sink = self.r.sum()
+
+    def describe(self):
+        return ("flushed before every timed step: 256 MiB written" +
+                (", then a second 256 MiB buffer read (write-back of the flush's dirty lines "
+                 "is outside the step)" if self.read_back else ""))
+
+
 def timed_steps(torch, fn, steps, flush):
     """Per-step CUDA-event times (ms) with an L2 flush before every step."""
     times = []
@@ -360,7 +383,7 @@ def run_ours(a):
         return run_cfg5(a, torch, dist, rank, world, dev)
     w = inputs.workload(a.workload)
     peaks, peaks_src = load_peaks()
-    flush = torch.empty(FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
+    flush = L2Flush(torch, dev)
 
     if slab:
         from paper_2601_18838_b200.dist import SlabPlan
@@ -455,7 +478,7 @@ def run_ours(a):
                         "parallelism": (f"rank grid {'x'.join(map(str, sp.dims))} of cell "
                                         f"blocks, one process per GPU, plan-owned NCCL core "
                                         f"all-reduce") if slab else "1 GPU",
-                        "l2": "flushed (256 MiB write) before every timed step",
+                        "l2": flush.describe(),
                         "timing": "CUDA events per step, max over ranks"},
         "e2e": {"value": w.n / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "ms_per_step_spread": e2e_spread,

@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libkpme_b200.so")
+# KPME_LIB: another build of the same library (A/B of kernel variants, scripts/build_variant.sh)
+LIB_PATH = os.environ.get("KPME_LIB") or os.path.join(HERE, "libkpme_b200.so")
 
 OK, INVALID_ARGUMENT, RUNTIME, NUMERICAL, CUDA, NCCL = range(6)
 FORM_AUTO, FORM_COLLAPSED, FORM_DENSE = 0, 1, 2

@@ -8,6 +8,7 @@
 // and each cell's grid accumulates in shared memory / registers: no global
 // atomics, and every sum runs in a fixed order (bit-identical re-runs).
 #include "internal.h"
+#include "trace.h"
 
 namespace kb {
 namespace {
@@ -989,6 +990,9 @@ __global__ void __launch_bounds__(32 * UV_NW, SPREAD_MINB) k_spread_uv(ColumnArg
 // L = 6 the B fragment of lane group g at n-tile t < 3 is U_g t0^t with
 // U_g = t1^jl t2^kl over (jl, kl) = (g / 3, g % 3), and tile 3 holds the
 // three (il, 2, 2) columns as W[g] = t0^g t1^2 t2^2.
+#ifndef F8_SKIP
+#define F8_SKIP 0  // profiling ablations only: 1 k-steps, 2 per-cell drain + contraction, 4 epilogue, 8 staging
+#endif
 #ifndef F8_RING
 #define F8_RING 2
 #endif
@@ -1074,6 +1078,7 @@ __global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_
     const int RP = uv_t1_stride(R), n2 = g.n[2];
     const ColumnRange cr = column_range(g, a.S);
     extern __shared__ double sm[];
+    TRACE_MARK(0, 0);
     const int per_warp = spread_f8_warp_doubles<L>(R);
     double* St = sm + warp * per_warp;  // [32][SR] staged particle rows
     double* ph = St + M::stage;         // [MT2*8][LDK] finished cell grid
@@ -1166,6 +1171,7 @@ __global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_
         cp_async_commit();
         pslot = pslot + 1 == M::RING ? 0 : pslot + 1;
     };
+    TRACE_MARK(0, 1);
 #pragma unroll
     for (int u = 0; u < M::RING - 1; ++u) issue();
     for (int c2 = zw0; c2 < zw1; ++c2) {
@@ -1194,7 +1200,9 @@ __global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_
             tmax = fmax(tmax, fmax(fabs(t0), fmax(fabs(t1), fabs(t2))));
             __syncwarp();  // previous chunk's fragment reads done
             double* row = St + lane * SR;
-            if (L == 6) {
+            if (F8_SKIP & 8) {
+                row[0] = t0 + t1 + t2 + q;
+            } else if (L == 6) {
                 const double a2 = t0 * t0, b2 = t1 * t1, c2v = t2 * t2;
                 const double T0 = a2 * t0, T1 = b2 * t1, T2 = c2v * t2;
                 const double qT1 = q * T1, qT0 = q * T0, qT0T1 = qT0 * T1;
@@ -1226,7 +1234,7 @@ __global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_
                 *reinterpret_cast<double2*>(row + 14) = make_double2(qab * c2v, t0 * b1c1);
             }
             __syncwarp();
-            const int ks = (cnt + 3) >> 2;
+            const int ks = (F8_SKIP & 1) ? 0 : (cnt + 3) >> 2;
             for (int kk = 0; kk < ks; ++kk) {
                 const double* r = St + (kk * 4 + tg) * SR;
                 const double2 au = *reinterpret_cast<const double2*>(r + 2 * gg);
@@ -1244,6 +1252,10 @@ __global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_
             }
         }
         __syncwarp();
+        if (F8_SKIP & 2) {
+            t1acc[0][0][0] += acc[0][0] + acc[NT - 1][1] + St[lane];
+            continue;
+        }
         // accumulator (g, 8t + 2c + e) -> ph[(i, j)][k]
 #pragma unroll
         for (int t = 0; t < NT; ++t)
@@ -1281,6 +1293,7 @@ __global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_
     }
     cp_async_wait<0>();
     __syncwarp();
+    TRACE_MARK(0, 2);
     if (want_fwd) {
         // the rows past MT2*8 stay zero: the epilogue reads only (i, j) < L^2
 #pragma unroll
@@ -1295,7 +1308,12 @@ __global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_
     // tensor_weights' out-of-cell check, |t| <= 1 + 2e-12 (slack 1e-12 of the width)
     const unsigned badw = __ballot_sync(0xffffffffu, !(tmax <= 1.0 + 2e-12));
     if (lane == 0 && badw) atomicOr(&a.bad[1], 1ull);
+    if (F8_SKIP & 4) {
+        if (a.Fpart && sm[threadIdx.x] + qsum == 1.2345) a.Fpart[0] = 0.0;
+        return;
+    }
     spread_epilogue<L, NW>(a, cr, sm, per_warp, t1off, RP, epi, red, qsum, want_fwd);
+    TRACE_MARK(0, 3);
 }
 
 // Records s, s + stride, ... of the sorted order for one gather thread: the
@@ -1359,6 +1377,7 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
     extern __shared__ double sm[];
     double* b2s = sm;             // L^2 x R
     double* psi = b2s + L2 * R;   // cells_per_batch x L^3
+    TRACE_MARK(1, 0);
     __shared__ double lc[16];
     __shared__ int gcst[kGatherTab + 1];
     __shared__ double4 gax[kGatherTab];
@@ -1419,6 +1438,7 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
     }
     const CellAxis ax0 = cell_axis_tab(a.cellax[0], cr.c0), ax1 = cell_axis_tab(a.cellax[1], cr.c1);
     __syncthreads();
+    TRACE_MARK(1, 1);
     double* w2s = psi + (size_t)cells_per_batch * L3 + (size_t)R * R * R + (size_t)L * R * R +
                   2 * (size_t)R * L;  // [R][cells_per_batch * L] W2 slice of the batch
     for (int cb0 = cr.zb; cb0 < cr.ze; cb0 += cells_per_batch) {
@@ -1494,6 +1514,7 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
             }
         }
         __syncthreads();
+        TRACE_MARK(1, 2);
         if (MONO && MODE != PSI_ONLY && !(GATHER_SKIP & 1) && cb1 - cb0 <= kGatherTab && !(GATHER_PAIRS && a.gpairs)) {
             // cell starts and z axes of the batch in shared memory; each thread
             // walks its particles in increasing order, so its cell only advances
@@ -1698,7 +1719,403 @@ __global__ void __launch_bounds__(GT, GATHER_MINB) k_bwd_gather_t(ColumnArgs a, 
             }
         }
         __syncthreads();
+        TRACE_MARK(1, 3);
     }
+}
+
+// ---- cell-chunk gather (the monomial hot path where cells hold >= 64 particles) ----
+// The nested-Horner gather above is bound by shared-memory wavefronts: every
+// lane reads all L^3 coefficients of its cell for each pair of particles, and a
+// warp of adjacent pairs spans two cells most of the time (ncu, config 3: 6.6
+// wavefronts per particle, data pipe 60% busy, FP64 pipe 32%). Here a warp takes
+// an exact quarter of the batch's particles and walks them cell by cell in
+// chunks of up to 128 from ONE cell: lane l evaluates particles l, l + 32,
+// l + 64, l + 96 of the chunk as up to four interleaved Horner chains, so each
+// coefficient is one broadcast read feeding up to 128 particles (about 2
+// wavefronts per particle at 108 per cell) and the chains hide the DFMA
+// latency. The records of the next chunk stream into a lane-private cp.async
+// ring (x, y as one 16-byte copy, z as one 8-byte copy) while the current one
+// is evaluated. Results, zero mode and the out-of-cell check are as above.
+#ifndef GATHER_CC
+#define GATHER_CC 1
+#endif
+constexpr int kCcChains = 4;
+constexpr int kCcChunk = 32 * kCcChains;
+constexpr int kCcStageDoubles = 4 * kCcChunk * 3;  // one ring stage: 4 warps x 128 x (x, y, z)
+// Shared-memory layout (doubles): b2s | psi | ring stage 0 | scratch | w2s. The
+// prologue scratch (G .* F, the x-expanded core, the W0 / W1 column rows) is
+// dead once b2s exists, so ring stage 1 lies on top of it; stage 0 is separate:
+// the first chunk's records are requested before the expansions run.
+__host__ __device__ constexpr int gather_cc_scratch_doubles(int L, int R) {
+    const int pro = R * R * R + L * R * R + 2 * R * L;
+    return pro > kCcStageDoubles ? pro : kCcStageDoubles;
+}
+// offsets rounded to 16 bytes (cp.async and the 128-bit coefficient reads)
+__host__ __device__ constexpr int gather_cc_psi_off(int L, int R) { return (L * L * R + 1) & ~1; }
+__host__ __device__ constexpr int gather_cc_ring_off(int L, int R, int cb) {
+    return gather_cc_psi_off(L, R) + ((cb * L * L * L + 1) & ~1);
+}
+__host__ __device__ constexpr int gather_cc_scr_off(int L, int R, int cb) {
+    return gather_cc_ring_off(L, R, cb) + kCcStageDoubles;
+}
+__host__ __device__ constexpr size_t gather_cc_smem_doubles(int L, int R, int cb) {
+    return (size_t)gather_cc_scr_off(L, R, cb) + (size_t)gather_cc_scratch_doubles(L, R) +
+           (size_t)R * cb * L;
+}
+
+// z[u] = sum_abc C[a][b][c] t0[u]^a t1[u]^b t2[u]^c for NCH particles of one cell
+// (nested Horner; the a loop is kept rolled: the body is already 36 NCH DFMAs)
+template <int L, int NCH>
+__device__ __forceinline__ void horner_chains(const double* __restrict__ ps, const double (&t0)[NCH],
+                                              const double (&t1)[NCH], const double (&t2)[NCH],
+                                              double (&z)[NCH]) {
+#pragma unroll
+    for (int u = 0; u < NCH; ++u) z[u] = 0.0;
+#pragma unroll 1
+    for (int i = L - 1; i >= 0; --i) {
+        double zb[NCH];
+        const double* rowi = ps + i * L * L;
+#pragma unroll
+        for (int j = L - 1; j >= 0; --j) {
+            const double* row = rowi + j * L;
+            double c[L];
+            if (L % 2 == 0) {
+#pragma unroll
+                for (int k = 0; k < L; k += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(row + k);
+                    c[k] = v.x;
+                    c[k + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < L; ++k) c[k] = row[k];
+            }
+            double zc[NCH];
+#pragma unroll
+            for (int u = 0; u < NCH; ++u) zc[u] = c[L - 1];
+#pragma unroll
+            for (int k = L - 2; k >= 0; --k)
+#pragma unroll
+                for (int u = 0; u < NCH; ++u) zc[u] = fma(zc[u], t2[u], c[k]);
+#pragma unroll
+            for (int u = 0; u < NCH; ++u) zb[u] = j == L - 1 ? zc[u] : fma(zb[u], t1[u], zc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < NCH; ++u) z[u] = fma(z[u], t0[u], zb[u]);
+    }
+}
+
+// One chunk: particles cbase + lane + 32 u (u < NCH) of the cell whose
+// coefficients are at ps; records from the lane's ring slots.
+template <int L, int NCH>
+__device__ __forceinline__ void gather_cc_chunk(const ColumnArgs& a, const double* __restrict__ ps,
+                                                const double2* __restrict__ rxy,
+                                                const double* __restrict__ rz, int cbase, int end,
+                                                int lane, const CellAxis& ax0, const CellAxis& ax1,
+                                                const double4& x2, double corr, double& tmax) {
+    double t0[NCH], t1[NCH], t2[NCH], z[NCH];
+    int dst[NCH];
+#pragma unroll
+    for (int u = 0; u < NCH; ++u) {
+        const int s = cbase + lane + 32 * u;
+        const bool ok = s < end;
+        dst[u] = ok ? __ldg(a.perm + s) : -1;
+        const double2 xy = rxy[lane + 32 * u];
+        const double zz = rz[lane + 32 * u];
+        t0[u] = ok ? (xy.x - ax0.mid) * ax0.inv : 0.0;
+        t1[u] = ok ? (xy.y - ax1.mid) * ax1.inv : 0.0;
+        t2[u] = ok ? (zz - x2.z) * x2.w : 0.0;
+        tmax = fmax(tmax, fmax(fabs(t0[u]), fmax(fabs(t1[u]), fabs(t2[u]))));
+    }
+    horner_chains<L, NCH>(ps, t0, t1, t2, z);
+#pragma unroll
+    for (int u = 0; u < NCH; ++u)
+        if (dst[u] >= 0) a.out[dst[u]] = z[u] - corr;
+}
+
+template <int L, int MINB, int RC>
+__global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells_per_batch) {
+    constexpr int L2 = L * L, L3 = L2 * L, NW = 4, NTH = 128;
+    const Geometry& g = a.g;
+    const int R = RC ? RC : g.R;  // RC: compile-time R (unrolled expansions), 0 = any R <= 16
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const ColumnRange cr = column_range(g, a.S);
+    extern __shared__ double sm[];
+    double* b2s = sm;                                         // [L^2][R]
+    double* psi = sm + gather_cc_psi_off(L, R);               // [cells_per_batch][L^3]
+    double* ring0 = sm + gather_cc_ring_off(L, R, cells_per_batch);
+    double* scr = sm + gather_cc_scr_off(L, R, cells_per_batch);  // prologue scratch, then ring stage 1
+    double* w2s = scr + gather_cc_scratch_doubles(L, R);      // [R][cells_per_batch * L]
+    __shared__ int gcst[kGatherTab + 1];
+    __shared__ double4 gax[kGatherTab];
+    TRACE_MARK(1, 0);
+    const int RR = R * R, R3 = RR * R;
+    double* h = scr;           // [R^3]  G .* F
+    double* v = h + R3;        // [L][R][R]
+    double* w01 = v + L * RR;  // [2][R][L]
+    // ring stage st of this warp: (x, y) pairs then z
+    auto stage_xy = [&](int st) { return reinterpret_cast<double2*>(st ? scr : ring0) + warp * kCcChunk; };
+    auto stage_z = [&](int st) { return (st ? scr : ring0) + NW * kCcChunk * 2 + warp * kCcChunk; };
+    const CellAxis ax0 = cell_axis_tab(a.cellax[0], cr.c0), ax1 = cell_axis_tab(a.cellax[1], cr.c1);
+    double corr = a.corr ? *a.corr : 0.0;
+    const bool fused = a.B2 == nullptr;
+    if (fused) corr = 0.0;
+    double tmax = 0.0;
+    for (int cb0 = cr.zb; cb0 < cr.ze; cb0 += cells_per_batch) {
+        const bool first = cb0 == cr.zb;
+        const int cb1 = min(cr.ze, cb0 + cells_per_batch), nb = cb1 - cb0;
+        const int cell0 = (cr.c0 * g.K[1] + cr.c1) * g.K[2] + cb0;
+        const int nz = nb * L;
+        {
+            // every global load of the batch's tables (and, in the first batch,
+            // of the column's core and W rows) is in flight before the first use
+            constexpr int WU = 16, HU = 6;  // R <= 16 rows of the W2 slice, one z column per thread
+            double wv[WU], gv[HU], fv[HU], wa = 0.0, wb = 0.0;
+            const bool w2_regs = nz <= NTH, h_regs = R3 <= NTH * HU;
+            if (w2_regs && tid < nz) {
+                const double* wsrc = a.W2 + cb0 * L + tid;
+#pragma unroll
+                for (int u = 0; u < WU; ++u)
+                    if (u < R) wv[u] = __ldg(wsrc + (int64_t)u * g.n[2]);
+            }
+            const int st0 = tid <= nb ? __ldg(a.start + cell0 + tid) : 0;
+            double4 axv = make_double4(0.0, 0.0, 0.0, 0.0);
+            if (tid < nb) axv = a.cellax[2][cb0 + tid];
+            double fq = 0.0;  // sum q (the last core entry), for the zero mode
+            if (first && fused) {
+                if (tid == 0) fq = __ldg(a.Fc + R3);
+                if (h_regs) {
+#pragma unroll
+                    for (int u = 0; u < HU; ++u) {
+                        const int e = tid + NTH * u;
+                        if (e < R3) {
+                            gv[u] = __ldg(a.Gc + e);
+                            fv[u] = __ldg(a.Fc + e);
+                        }
+                    }
+                }
+                if (tid < R * L) {
+                    wa = a.W0[(int64_t)(tid / L) * g.n[0] + cr.c0 * L + tid % L];
+                    wb = a.W1[(int64_t)(tid / L) * g.n[1] + cr.c1 * L + tid % L];
+                }
+            }
+            if (tid <= nb) gcst[tid] = st0;
+            if (tid < nb) gax[tid] = axv;
+            if (w2_regs) {
+                if (tid < nz) {
+#pragma unroll
+                    for (int u = 0; u < WU; ++u)
+                        if (u < R) w2s[u * nz + tid] = wv[u];
+                }
+            } else {
+                for (int e = tid; e < R * nz; e += NTH)
+                    w2s[e] = __ldg(a.W2 + (int64_t)(e / nz) * g.n[2] + cb0 * L + e % nz);
+            }
+            if (first && fused) {
+                // zero mode, exactly: h[0] = (G[0] - c) sum q
+                if (h_regs) {
+#pragma unroll
+                    for (int u = 0; u < HU; ++u)
+                        if (tid + NTH * u < R3)
+                            h[tid + NTH * u] = (u == 0 && tid == 0) ? (gv[0] - a.correction) * fq : gv[u] * fv[u];
+                } else {
+                    for (int e = tid; e < R3; e += NTH)
+                        h[e] = e == 0 ? (__ldg(a.Gc) - a.correction) * fq : __ldg(a.Gc + e) * __ldg(a.Fc + e);
+                }
+                if (tid < R * L) {
+                    w01[tid] = wa;
+                    w01[R * L + tid] = wb;
+                }
+                for (int e = NTH + tid; e < R * L; e += NTH) {  // R * L > 128 only for R > 16
+                    w01[e] = a.W0[(int64_t)(e / L) * g.n[0] + cr.c0 * L + e % L];
+                    w01[R * L + e] = a.W1[(int64_t)(e / L) * g.n[1] + cr.c1 * L + e % L];
+                }
+            } else if (first) {
+                for (int e = tid; e < L2 * R; e += NTH) {
+                    const int ij = e / R, r = e % R, i = ij / L, j = ij % L;
+                    b2s[e] = a.B2[((int64_t)(cr.c0 * L + i) * g.n[1] + cr.c1 * L + j) * R + r];
+                }
+            }
+        }
+        __syncthreads();
+        if (first) TRACE_MARK(1, 7);
+        // The warp's particle range of this batch and its first chunk's records:
+        // requested now, they arrive while the expansions below run.
+        const int P0 = gcst[0], P1 = gcst[nb];
+        const int pw0 = P0 + (int)((long long)(P1 - P0) * warp / NW);
+        const int pw1 = P0 + (int)((long long)(P1 - P0) * (warp + 1) / NW);
+        int cc = 0, pc = 0, pbase = pw0, cbase = pw0, pslot = 0, cslot = 0;
+        if (pw0 < pw1) {
+            while (gcst[cc + 1] <= pw0) ++cc;
+            pc = cc;
+        }
+        auto issue = [&]() {
+            if (pbase < pw1) {
+                const int end = min(pbase + kCcChunk, min(gcst[pc + 1], pw1));
+                double2* dxy = stage_xy(pslot);
+                double* dz = stage_z(pslot);
+#pragma unroll
+                for (int u = 0; u < kCcChains; ++u) {
+                    const int s = pbase + lane + 32 * u;
+                    if (s < end) {
+                        const char* src = reinterpret_cast<const char*>(a.sp + s);
+                        cp_async16_sm(dxy + lane + 32 * u, src);
+                        cp_async8_sm(dz + lane + 32 * u, src + 16);
+                    }
+                }
+                pbase = end;
+                while (pbase < pw1 && pbase >= gcst[pc + 1]) ++pc;
+            }
+            cp_async_commit();
+            pslot ^= 1;
+        };
+        issue();  // stage 0 (never aliased)
+        if (first && fused) {
+            // fused backward y, x expansions (the U_0, U_1 phases of spkmv) for this column
+            if constexpr (RC > 0) {
+                // every thread's outputs at once: the loads of all of them are in flight together
+                constexpr int NV = L * RC * RC, IT = (NV + NTH - 1) / NTH;
+                double sv[IT];
+#pragma unroll
+                for (int it = 0; it < IT; ++it) {
+                    const int e = min(tid + it * NTH, NV - 1);
+                    const int i = e / (RC * RC), rr = e % (RC * RC);
+                    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                    for (int r0 = 0; r0 < RC; r0 += 2) {
+                        s0 = fma(w01[r0 * L + i], h[r0 * RC * RC + rr], s0);
+                        if (r0 + 1 < RC) s1 = fma(w01[(r0 + 1) * L + i], h[(r0 + 1) * RC * RC + rr], s1);
+                    }
+                    sv[it] = s0 + s1;
+                }
+#pragma unroll
+                for (int it = 0; it < IT; ++it)
+                    if (tid + it * NTH < NV) v[tid + it * NTH] = sv[it];
+            } else {
+                for (int e = tid; e < L * RR; e += NTH) {
+                    const int i = e / RR, rr = e % RR;
+                    double s = 0.0;
+                    for (int r0 = 0; r0 < R; ++r0) s = fma(w01[r0 * L + i], h[r0 * RR + rr], s);
+                    v[e] = s;
+                }
+            }
+            __syncthreads();
+            TRACE_MARK(1, 8);
+            if constexpr (RC > 0) {
+                constexpr int NB = L2 * RC, IT = (NB + NTH - 1) / NTH;
+                double sv[IT];
+#pragma unroll
+                for (int it = 0; it < IT; ++it) {
+                    const int e = min(tid + it * NTH, NB - 1);
+                    const int ij = e / RC, r2 = e % RC, i = ij / L, j = ij % L;
+                    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                    for (int r1 = 0; r1 < RC; r1 += 2) {
+                        s0 = fma(w01[RC * L + r1 * L + j], v[i * RC * RC + r1 * RC + r2], s0);
+                        if (r1 + 1 < RC)
+                            s1 = fma(w01[RC * L + (r1 + 1) * L + j], v[i * RC * RC + (r1 + 1) * RC + r2], s1);
+                    }
+                    sv[it] = s0 + s1;
+                }
+#pragma unroll
+                for (int it = 0; it < IT; ++it)
+                    if (tid + it * NTH < NB) b2s[tid + it * NTH] = sv[it];
+            } else {
+                for (int e = tid; e < L2 * R; e += NTH) {
+                    const int ij = e / R, r2 = e % R, i = ij / L, j = ij % L;
+                    double s = 0.0;
+                    for (int r1 = 0; r1 < R; ++r1) s = fma(w01[R * L + r1 * L + j], v[i * RR + r1 * R + r2], s);
+                    b2s[e] = s;
+                }
+            }
+        }
+        if (first) {
+            __syncthreads();
+            TRACE_MARK(1, 1);
+        }
+        {
+            // psi_cell[(i,j)][k] = sum_r B2col[(i,j)][r] W2[r][c2 L + k] on DMMA (R <= 16).
+            // Row r = 0 of the monomial W2 is exactly (1, 0, ..., 0) in every cell
+            // (k_factor_wl), so it adds B2col[(i,j)][0] at k = 0 and the product
+            // runs over r = 1 .. R-1 (R = 9: two k-steps, no padding).
+            constexpr int MT = (L2 + 7) / 8, KSMAX = RC ? (RC + 2) / 4 : 4;
+            const int R1 = R - 1, KS = (R1 + 3) / 4;
+            double af[MT][KSMAX], b0[MT];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const int row = mt * 8 + (lane >> 2);
+                b0[mt] = ((lane & 3) == 0 && row < L2) ? b2s[row * R] : 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KSMAX; ++ks) {
+                    const int r = ks * 4 + (lane & 3);
+                    af[mt][ks] = (ks < KS && row < L2 && r < R1) ? b2s[row * R + 1 + r] : 0.0;
+                }
+            }
+            for (int b = warp; b < nb; b += NW) {
+                double bf[KSMAX];
+#pragma unroll
+                for (int ks = 0; ks < KSMAX; ++ks) {
+                    const int r = ks * 4 + (lane & 3), k = lane >> 2;
+                    bf[ks] = (ks < KS && r < R1 && k < L) ? w2s[(1 + r) * nz + b * L + k] : 0.0;
+                }
+                double* ps = psi + b * L3;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    double c[2] = {b0[mt], 0.0};
+#pragma unroll
+                    for (int ks = 0; ks < KSMAX; ++ks)
+                        if (ks < KS) dmma884(c, af[mt][ks], bf[ks]);
+                    const int row = mt * 8 + (lane >> 2), k0 = 2 * (lane & 3);
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2)
+                        if (row < L2 && k0 + q2 < L) {
+                            ps[row * L + k0 + q2] = c[q2];
+                            if (a.psi_cells)
+                                a.psi_cells[(int64_t)(cell0 + b) * L3 + row * L + k0 + q2] = c[q2];
+                        }
+                }
+            }
+        }
+        __syncthreads();  // psi complete; the scratch is free for ring stage 1
+        TRACE_MARK(1, 2);
+        if (pw0 < pw1) {
+            TRACE_DECL(tr_wait);
+            TRACE_DECL(tr_work);
+            TRACE_DECL(tr_chunks);
+            while (cbase < pw1) {
+                const int end = min(cbase + kCcChunk, min(gcst[cc + 1], pw1));
+                TRACE_CLK(tr0);
+                issue();
+                cp_async_wait<1>();
+                TRACE_CLK(tr1);
+                const double* ps = psi + cc * L3;
+                const double4 x2 = gax[cc];  // (lo, hi, mid, inv)
+                const double2* cxy = stage_xy(cslot);
+                const double* cz = stage_z(cslot);
+                switch ((end - cbase + 31) >> 5) {
+                    case 1: gather_cc_chunk<L, 1>(a, ps, cxy, cz, cbase, end, lane, ax0, ax1, x2, corr, tmax); break;
+                    case 2: gather_cc_chunk<L, 2>(a, ps, cxy, cz, cbase, end, lane, ax0, ax1, x2, corr, tmax); break;
+                    case 3: gather_cc_chunk<L, 3>(a, ps, cxy, cz, cbase, end, lane, ax0, ax1, x2, corr, tmax); break;
+                    default: gather_cc_chunk<L, 4>(a, ps, cxy, cz, cbase, end, lane, ax0, ax1, x2, corr, tmax);
+                }
+                TRACE_CLK(tr2);
+                TRACE_ACC(tr_wait, tr0, tr1);
+                TRACE_ACC(tr_work, tr1, tr2);
+                TRACE_ACC(tr_chunks, 0, (end - cbase + 31) >> 5);
+                cslot ^= 1;
+                cbase = end;
+                while (cbase < pw1 && cbase >= gcst[cc + 1]) ++cc;
+            }
+            TRACE_PUT(1, 4, tr_wait);
+            TRACE_PUT(1, 5, tr_work);
+            TRACE_PUT(1, 6, tr_chunks);
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+        TRACE_MARK(1, 3);
+    }
+    // tensor_weights' out-of-cell check, |t| <= 1 + 2e-12 (slack 1e-12 of the width)
+    if (__ballot_sync(0xffffffffu, !(tmax <= 1.0 + 2e-12)) && lane == 0) atomicOr(&a.bad[1], 1ull);
 }
 
 size_t spread_smem(const Geometry& g) {
@@ -1851,6 +2268,43 @@ void launch_gather_t(const ColumnArgs& a0, int mode, cudaStream_t s) {
     const size_t smem = sizeof(double) * ((size_t)L * L * R + (size_t)cb * L * L * L +
                                           (size_t)R * R * R + (size_t)L * R * R +
                                           2 * (size_t)R * L + (size_t)R * cb * L);
+    if constexpr (L == 4 || L == 6 || L == 8) {
+        // cell-chunk gather: the monomial hot path where cells are full enough
+        // (the plan's gpairs flag: >= 64 particles per cell on average)
+        static const int cc_env = [] {
+            const char* e = getenv("KPME_GATHER_CC");
+            return e ? atoi(e) : -1;
+        }();
+        const bool cc_on = cc_env >= 0 ? cc_env != 0 : a.gpairs != 0;
+        if (GATHER_CC && cc_on && mode == GATHER_FROM_B2 && a.mono && R <= 16 && !a.direct) {
+            const int ccb = std::min(cb, kGatherTab);
+            const size_t csm = sizeof(double) * gather_cc_smem_doubles(L, R, ccb);
+            if (csm <= 200 * 1024) {
+                static PerDevice cc_once;
+                once_per_device(cc_once, [&] {
+                    KB_CUDA(cudaFuncSetAttribute(k_gather_cc<L, 3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 200 * 1024));
+                    KB_CUDA(cudaFuncSetAttribute(k_gather_cc<L, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 200 * 1024));
+                    KB_CUDA(cudaFuncSetAttribute(k_gather_cc<L, 3, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 200 * 1024));
+                    KB_CUDA(cudaFuncSetAttribute(k_gather_cc<L, 4, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 200 * 1024));
+                });
+                const bool waves = grid > 2 * 3 * sm_count() && csm * 4 <= 220 * 1024;
+                if (R == 9 && waves)
+                    k_gather_cc<L, 4, 9><<<grid, 128, csm, s>>>(a, ccb);
+                else if (R == 9)
+                    k_gather_cc<L, 3, 9><<<grid, 128, csm, s>>>(a, ccb);
+                else if (waves)
+                    k_gather_cc<L, 4, 0><<<grid, 128, csm, s>>>(a, ccb);
+                else
+                    k_gather_cc<L, 3, 0><<<grid, 128, csm, s>>>(a, ccb);
+                KB_CHECK_LAUNCH();
+                return;
+            }
+        }
+    }
     switch (mode) {
         case GATHER_FROM_B2:
             if (a.mono && L <= 8)
@@ -1949,3 +2403,5 @@ void launch_bwd_gather(const ColumnArgs& a, int mode, cudaStream_t s) {
 }
 
 }  // namespace kb
+
+TRACE_READER(interp)

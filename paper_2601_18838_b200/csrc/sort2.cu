@@ -24,6 +24,7 @@
 #include <type_traits>
 
 #include "internal.h"
+#include "trace.h"
 
 namespace kb {
 namespace {
@@ -418,6 +419,7 @@ __device__ __forceinline__ void z_whole_core(const Geometry& g, int col, int cs,
     }
     __syncthreads();
     ZSTAMP();
+    TRACE_MARK(1, 3);
     // 3: exclusive scan of the counters in (c2, thread) order: thread t scans
     // the K2 consecutive entries [t*K2, (t+1)*K2)
     {
@@ -442,6 +444,7 @@ __device__ __forceinline__ void z_whole_core(const Geometry& g, int col, int cs,
     }
     __syncthreads();
     ZSTAMP();
+    TRACE_MARK(1, 4);
     for (int z = tid; z < K2; z += kZThreads) start[(int64_t)col * K2 + z] = cs + cnt[z * kZThreads];
     if (col == ncol - 1 && tid == 0) start[(int64_t)ncol * K2] = (int)n;
     // 4: stable ranks -> inverse permutation (running 4-bit counters again)
@@ -460,6 +463,7 @@ __device__ __forceinline__ void z_whole_core(const Geometry& g, int col, int cs,
     }
     __syncthreads();
     ZSTAMP();
+    TRACE_MARK(1, 5);
     // 5: the column leaves in cell order as one contiguous run
     emit(s_inv);
 #ifdef ZSORT_PROFILE
@@ -1091,6 +1095,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, KEYS_MINB) k_tile_keys(Geomet
     int32_t* tc = reinterpret_cast<int32_t*>(tsm + TL.tc);
     int32_t* cb = reinterpret_cast<int32_t*>(tsm + TL.cb);
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    TRACE_MARK(0, 0);
     for (int e = tid; e < (int)((TL.tc - TL.wc) / 16); e += blockDim.x)
         reinterpret_cast<uint4*>(wc)[e] = make_uint4(0u, 0u, 0u, 0u);
     const int64_t tbase = (int64_t)blockIdx.x * kTT;
@@ -1127,6 +1132,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, KEYS_MINB) k_tile_keys(Geomet
         }
     }
     __syncthreads();
+    TRACE_MARK(0, 1);
     unsigned pk[TR];
 #pragma unroll
     for (int r = 0; r < TR; ++r) {
@@ -1138,6 +1144,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, KEYS_MINB) k_tile_keys(Geomet
         __syncwarp();
     }
     __syncthreads();
+    TRACE_MARK(0, 2);
     for (int c = tid; c < ncol; c += blockDim.x) {
         int run = 0;
 #pragma unroll
@@ -1150,6 +1157,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, KEYS_MINB) k_tile_keys(Geomet
     }
     __syncthreads();
     block_col_bases(tc, ncol, cb, wsum);
+    TRACE_MARK(0, 3);
     int32_t* trow = toff + (int64_t)blockIdx.x * (ncol + 1);
     for (int c = tid; c <= ncol; c += blockDim.x) trow[c] = cb[c];
 #pragma unroll
@@ -1167,8 +1175,10 @@ __global__ void __launch_bounds__(kTileWarps * 32, KEYS_MINB) k_tile_keys(Geomet
         __syncwarp();
     }
     __syncthreads();
+    TRACE_MARK(0, 4);
     const int tn = cb[ncol];
     for (int k = tid; k < tn; k += blockDim.x) pairs[tbase + k] = s_pair[k];
+    TRACE_MARK(0, 5);
 }
 
 __device__ __forceinline__ void cp_async8_s(void* dst, const void* src) {
@@ -1212,6 +1222,7 @@ __global__ void __launch_bounds__(kZThreads, ZKO_MINB) k_z_tiles_ko(Geometry g, 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int per = (ntiles + kZThreads - 1) / kZThreads;
     const int lo = min(ntiles, tid * per), hi = min(ntiles, lo + per);
+    TRACE_MARK(1, 0);
     int a_[4], e_[4];
     int csum = 0, psum = 0;
     if (per <= 4) {
@@ -1268,6 +1279,7 @@ __global__ void __launch_bounds__(kZThreads, ZKO_MINB) k_z_tiles_ko(Geometry g, 
                                start, sp, zsm);
         return;
     }
+    TRACE_MARK(1, 1);
     const ZPairsLayout L(K2, whole_cap);
     int2* s_pair = reinterpret_cast<int2*>(zsm + L.pair);
     uint16_t* s_inv = reinterpret_cast<uint16_t*>(zsm + L.inv);
@@ -1295,8 +1307,10 @@ __global__ void __launch_bounds__(kZThreads, ZKO_MINB) k_z_tiles_ko(Geometry g, 
     for (int e = tid; e < K2 * kZThreads; e += kZThreads) cnt[e] = 0;
     cp_async_wait_all();
     __syncthreads();
+    TRACE_MARK(1, 2);
     z_whole_pairs<(ZB <= 6 ? ZB : 6)>(g, col, cs, m, n, s_pair, s_inv, s_z, cnt, perm, start, xyz, q, sp,
                                       wsum);
+    TRACE_MARK(1, 6);
 }
 
 // Instantiation for an even key width in [2, 16].
@@ -1516,3 +1530,5 @@ void launch_sort2(const Geometry& g, int64_t n, const double* xyz, const SortBuf
 }
 
 }  // namespace kb
+
+TRACE_READER(sort2)

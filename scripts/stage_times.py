@@ -15,9 +15,12 @@ for name in sys.argv[1:]:
     plan.execute(xyz, q, o, defer_checks=bool(os.environ.get("PROFILE_NOCHECK")))
     plan.enable_timing(True)
     flush = torch.empty(256 << 17, dtype=torch.float64, device='cuda')
+    flush_r = torch.zeros(256 << 17, dtype=torch.float64, device='cuda')  # read after the write: L2 ends clean (bench.py L2Flush)
     acc = None
     for _ in range(10):
         flush.zero_()
+        if os.environ.get("KPME_BENCH_FLUSH_READ", "1") != "0":
+            sink = flush_r.sum()
         plan.execute(xyz, q, o, defer_checks=True)
         st = plan.stage_times()
         acc = st if acc is None else [a + b for a, b in zip(acc, st)]

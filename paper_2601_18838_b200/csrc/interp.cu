@@ -993,6 +993,9 @@ __global__ void __launch_bounds__(32 * UV_NW, SPREAD_MINB) k_spread_uv(ColumnArg
 #ifndef F8_SKIP
 #define F8_SKIP 0  // profiling ablations only: 1 k-steps, 2 per-cell drain + contraction, 4 epilogue, 8 staging
 #endif
+#ifndef F8_NW
+#define F8_NW 4  // warps per column CTA of the split-exponent spread
+#endif
 #ifndef F8_RING
 #define F8_RING 2
 #endif
@@ -1061,7 +1064,7 @@ __host__ __device__ constexpr int spread_f8_warp_doubles(int R) {
 }
 template <int L>
 __host__ __device__ constexpr size_t spread_f8_smem_doubles(int R, int /*n2*/) {
-    return 4 * (size_t)spread_f8_warp_doubles<L>(R) + (size_t)spread_epilogue_doubles(L, R);
+    return F8_NW * (size_t)spread_f8_warp_doubles<L>(R) + (size_t)spread_epilogue_doubles(L, R);
 }
 
 // MINB: CTAs per SM the register allocation is sized for. 3 (162 registers)
@@ -1069,12 +1072,15 @@ __host__ __device__ constexpr size_t spread_f8_smem_doubles(int R, int /*n2*/) {
 // columns, 45.2 vs 47.6 us at 4); 4 (128 registers, a few spilled bytes) for
 // grids of several waves (config 4: 1849 columns, 173.5 vs 179.8 us).
 template <int L, int RTM, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_fwd) {
+__global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, int want_fwd) {
     using M = F8Map<L>;
     constexpr int L3 = L * L * L, NT = M::NT, MT2 = M::MT2, KS2 = M::KS2, LDK = M::LDK, SR = M::SR;
-    constexpr int NW = 4, NTH = 128;
+    constexpr int NW = F8_NW, NTH = 32 * F8_NW;
     const Geometry& g = a.g;
-    const int R = g.R, RT = (R + 7) / 8, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // The monomial W2's row r = 0 is exactly (1, 0, ..., 0) in every cell (k_factor_wl), so
+    // T1[(i,j)][0] is the k = 0 entry of the cell grid: the W2 contraction runs over
+    // r = 1 .. R-1 (R = 9: one n-tile instead of two) and r = 0 is a running sum.
+    const int R = g.R, RT = (R - 1 + 7) / 8, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int RP = uv_t1_stride(R), n2 = g.n[2];
     const ColumnRange cr = column_range(g, a.S);
     extern __shared__ double sm[];
@@ -1098,6 +1104,10 @@ __global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_
     const int gg = lane >> 2, tg = lane & 3;
     double tmax = 0.0, qsum = 0.0;
     double t1acc[MT2][RTM][2];
+    constexpr int NR0 = (MT2 * 8 + 31) / 32;
+    double t1r0[NR0];
+#pragma unroll
+    for (int u = 0; u < NR0; ++u) t1r0[u] = 0.0;
 #pragma unroll
     for (int mt = 0; mt < MT2; ++mt)
 #pragma unroll
@@ -1276,9 +1286,12 @@ __global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_
             for (int s = 0; s < KS2; ++s)
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
-                    const int k = s * 4 + (lane & 3), rr = t * 8 + (lane >> 2);
+                    const int k = s * 4 + (lane & 3), rr = 1 + t * 8 + (lane >> 2);
                     bf[s][t] = (t < RT && k < L && rr < R) ? __ldg(w2c + (int64_t)rr * n2 + k) : 0.0;
                 }
+#pragma unroll
+            for (int u = 0; u < NR0; ++u)
+                if (lane + 32 * u < MT2 * 8) t1r0[u] += ph[(lane + 32 * u) * LDK];
 #pragma unroll
             for (int mt = 0; mt < MT2; ++mt)
 #pragma unroll
@@ -1300,9 +1313,15 @@ __global__ void __launch_bounds__(128, MINB) k_spread_f8(ColumnArgs a, int want_
         for (int mt = 0; mt < MT2; ++mt)
 #pragma unroll
             for (int t = 0; t < RTM; ++t)
-                if (t < RT)
-                    *reinterpret_cast<double2*>(t1w + (mt * 8 + (lane >> 2)) * RP + t * 8 + 2 * (lane & 3)) =
-                        make_double2(t1acc[mt][t][0], t1acc[mt][t][1]);
+                if (t < RT) {
+                    const int r = 1 + t * 8 + 2 * (lane & 3);
+                    double* dst = t1w + (mt * 8 + (lane >> 2)) * RP;
+                    if (r < R) dst[r] = t1acc[mt][t][0];
+                    if (r + 1 < R) dst[r + 1] = t1acc[mt][t][1];
+                }
+#pragma unroll
+        for (int u = 0; u < NR0; ++u)
+            if (lane + 32 * u < MT2 * 8) t1w[(lane + 32 * u) * RP] = t1r0[u];
         __syncwarp();
     }
     // tensor_weights' out-of-cell check, |t| <= 1 + 2e-12 (slack 1e-12 of the width)
@@ -1812,7 +1831,8 @@ __device__ __forceinline__ void gather_cc_chunk(const ColumnArgs& a, const doubl
                                                 const double2* __restrict__ rxy,
                                                 const double* __restrict__ rz, int cbase, int end,
                                                 int lane, const CellAxis& ax0, const CellAxis& ax1,
-                                                const double4& x2, double corr, double& tmax) {
+                                                const double4& x2, double corr, double& tmax,
+                                                long long* hacc = nullptr) {
     double t0[NCH], t1[NCH], t2[NCH], z[NCH];
     int dst[NCH];
 #pragma unroll
@@ -1827,7 +1847,12 @@ __device__ __forceinline__ void gather_cc_chunk(const ColumnArgs& a, const doubl
         t2[u] = ok ? (zz - x2.z) * x2.w : 0.0;
         tmax = fmax(tmax, fmax(fabs(t0[u]), fmax(fabs(t1[u]), fabs(t2[u]))));
     }
+    TRACE_CLK(h0);
     horner_chains<L, NCH>(ps, t0, t1, t2, z);
+    TRACE_CLK(h1);
+#ifdef KB_TRACE
+    if (hacc) *hacc += h1 - h0;
+#endif
 #pragma unroll
     for (int u = 0; u < NCH; ++u)
         if (dst[u] >= 0) a.out[dst[u]] = z[u] - corr;
@@ -2000,7 +2025,6 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
                 }
             }
             __syncthreads();
-            TRACE_MARK(1, 8);
             if constexpr (RC > 0) {
                 constexpr int NB = L2 * RC, IT = (NB + NTH - 1) / NTH;
                 double sv[IT];
@@ -2082,6 +2106,7 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
             TRACE_DECL(tr_wait);
             TRACE_DECL(tr_work);
             TRACE_DECL(tr_chunks);
+            TRACE_DECL(tr_horner);
             while (cbase < pw1) {
                 const int end = min(cbase + kCcChunk, min(gcst[cc + 1], pw1));
                 TRACE_CLK(tr0);
@@ -2093,10 +2118,10 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
                 const double2* cxy = stage_xy(cslot);
                 const double* cz = stage_z(cslot);
                 switch ((end - cbase + 31) >> 5) {
-                    case 1: gather_cc_chunk<L, 1>(a, ps, cxy, cz, cbase, end, lane, ax0, ax1, x2, corr, tmax); break;
-                    case 2: gather_cc_chunk<L, 2>(a, ps, cxy, cz, cbase, end, lane, ax0, ax1, x2, corr, tmax); break;
-                    case 3: gather_cc_chunk<L, 3>(a, ps, cxy, cz, cbase, end, lane, ax0, ax1, x2, corr, tmax); break;
-                    default: gather_cc_chunk<L, 4>(a, ps, cxy, cz, cbase, end, lane, ax0, ax1, x2, corr, tmax);
+                    case 1: gather_cc_chunk<L, 1>(a, ps, cxy, cz, cbase, end, lane, ax0, ax1, x2, corr, tmax, TRACE_PTR(tr_horner)); break;
+                    case 2: gather_cc_chunk<L, 2>(a, ps, cxy, cz, cbase, end, lane, ax0, ax1, x2, corr, tmax, TRACE_PTR(tr_horner)); break;
+                    case 3: gather_cc_chunk<L, 3>(a, ps, cxy, cz, cbase, end, lane, ax0, ax1, x2, corr, tmax, TRACE_PTR(tr_horner)); break;
+                    default: gather_cc_chunk<L, 4>(a, ps, cxy, cz, cbase, end, lane, ax0, ax1, x2, corr, tmax, TRACE_PTR(tr_horner));
                 }
                 TRACE_CLK(tr2);
                 TRACE_ACC(tr_wait, tr0, tr1);
@@ -2109,6 +2134,7 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
             TRACE_PUT(1, 4, tr_wait);
             TRACE_PUT(1, 5, tr_work);
             TRACE_PUT(1, 6, tr_chunks);
+            TRACE_PUT(1, 8, tr_horner);
         }
         cp_async_wait<0>();
         __syncthreads();
@@ -2180,6 +2206,10 @@ bool launch_spread_f8_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
         if (!SPREAD_F8 || smem > 200 * 1024 || a.g.R > 32) return false;
         static PerDevice attr_once;
         once_per_device(attr_once, [&] {
+            KB_CUDA(cudaFuncSetAttribute(k_spread_f8<L, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         200 * 1024));
+            KB_CUDA(cudaFuncSetAttribute(k_spread_f8<L, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         200 * 1024));
             KB_CUDA(cudaFuncSetAttribute(k_spread_f8<L, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          200 * 1024));
             KB_CUDA(cudaFuncSetAttribute(k_spread_f8<L, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2189,12 +2219,17 @@ bool launch_spread_f8_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
         });
         const int grid = block_columns(a.g) * a.S;
         const bool waves = grid > 2 * 3 * sm_count() && smem * 4 <= 220 * 1024;
-        if (a.g.R <= 16 && waves)
-            k_spread_f8<L, 2, 4><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
-        else if (a.g.R <= 16)
-            k_spread_f8<L, 2, 3><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+        // n-tiles of the W2 contraction over r = 1 .. R-1
+        if (a.g.R <= 9 && waves)
+            k_spread_f8<L, 1, 4><<<grid, 32 * F8_NW, smem, s>>>(a, want_fwd ? 1 : 0);
+        else if (a.g.R <= 9)
+            k_spread_f8<L, 1, 3><<<grid, 32 * F8_NW, smem, s>>>(a, want_fwd ? 1 : 0);
+        else if (a.g.R <= 17 && waves)
+            k_spread_f8<L, 2, 4><<<grid, 32 * F8_NW, smem, s>>>(a, want_fwd ? 1 : 0);
+        else if (a.g.R <= 17)
+            k_spread_f8<L, 2, 3><<<grid, 32 * F8_NW, smem, s>>>(a, want_fwd ? 1 : 0);
         else
-            k_spread_f8<L, 4, 3><<<grid, 128, smem, s>>>(a, want_fwd ? 1 : 0);
+            k_spread_f8<L, 4, 3><<<grid, 32 * F8_NW, smem, s>>>(a, want_fwd ? 1 : 0);
         KB_CHECK_LAUNCH();
         return true;
     } else {

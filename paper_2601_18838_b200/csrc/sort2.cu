@@ -495,6 +495,18 @@ __device__ __forceinline__ void z_whole_body(const Geometry& g, int col, int cs,
         s_inv, s_z, cnt, start, wsum);
 }
 
+// Record i from the input arrays with two loads for (x, y, z): the 24-byte
+// triple is either 16-byte aligned ((x, y) as one 128-bit load, then z) or 8
+// bytes past ((y, z) as the 128-bit load after x), decided on the address. A scattered warp load costs one
+// L1 wavefront per lane, so this is 3 instead of 4 per record with q.
+__device__ __forceinline__ double4 gather_rec(const double* __restrict__ xyz, const double* __restrict__ q,
+                                              int64_t i) {
+    const double* base = xyz + 3 * i;
+    const int odd = (int)((reinterpret_cast<uintptr_t>(base) >> 3) & 1);
+    const double2 v = __ldg(reinterpret_cast<const double2*>(base + odd));
+    const double s = __ldg(base + (odd ? 0 : 2));
+    return make_double4(odd ? s : v.x, odd ? v.x : v.y, odd ? v.y : s, q ? __ldg(q + i) : 0.0);
+}
 // The key path (k_z_tiles_ko): staged (particle, c2) pairs; the records are
 // gathered from the input arrays (L2-resident after the tile pass) straight
 // into their sorted place, four at a time per thread.
@@ -518,11 +530,7 @@ __device__ __forceinline__ void z_whole_pairs(const Geometry& g, int col, int cs
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
-                    if (sp && id[u] >= 0) {
-                        const int64_t i = id[u];
-                        r[u] = make_double4(__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1),
-                                            __ldg(xyz + 3 * i + 2), __ldg(q + i));
-                    }
+                    if (sp && id[u] >= 0) r[u] = gather_rec(xyz, q, id[u]);
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
                     if (id[u] >= 0) {
@@ -609,10 +617,7 @@ struct PairAcc {
     const double* q;
     __device__ int z(int64_t sj) const { return __ldg(&pairs[sj].y); }
     __device__ int idx(int64_t sj) const { return __ldg(&pairs[sj].x); }
-    __device__ double4 rec(int64_t, int i) const {
-        return make_double4(__ldg(xyz + 3 * (int64_t)i), __ldg(xyz + 3 * (int64_t)i + 1),
-                            __ldg(xyz + 3 * (int64_t)i + 2), q ? __ldg(q + i) : 0.0);
-    }
+    __device__ double4 rec(int64_t, int i) const { return gather_rec(xyz, q, i); }
 };
 template <int ZB, class Src, class Acc>
 __device__ __forceinline__ void z_sort_chunked_acc(const Geometry& g, int col, int cs, int m, Src src,
@@ -1158,8 +1163,9 @@ __global__ void __launch_bounds__(kTileWarps * 32, KEYS_MINB) k_tile_keys(Geomet
     __syncthreads();
     block_col_bases(tc, ncol, cb, wsum);
     TRACE_MARK(0, 3);
-    int32_t* trow = toff + (int64_t)blockIdx.x * (ncol + 1);
-    for (int c = tid; c <= ncol; c += blockDim.x) trow[c] = cb[c];
+    // column-major offsets toff[c][tile]: a column CTA of the second pass reads
+    // its two rows as contiguous runs (one scattered 4-byte store per column here)
+    for (int c = tid; c <= ncol; c += blockDim.x) toff[(int64_t)c * gridDim.x + blockIdx.x] = cb[c];
 #pragma unroll
     for (int r = 0; r < TR; ++r) {
         const bool act = colr[r] >= 0;
@@ -1229,8 +1235,8 @@ __global__ void __launch_bounds__(kZThreads, ZKO_MINB) k_z_tiles_ko(Geometry g, 
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if (lo + u < hi) {
-                a_[u] = __ldg(toff + (int64_t)(lo + u) * (ncol + 1) + col);
-                e_[u] = __ldg(toff + (int64_t)(lo + u) * (ncol + 1) + col + 1);
+                a_[u] = __ldg(toff + (int64_t)col * ntiles + lo + u);
+                e_[u] = __ldg(toff + (int64_t)(col + 1) * ntiles + lo + u);
             }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -1240,9 +1246,9 @@ __global__ void __launch_bounds__(kZThreads, ZKO_MINB) k_z_tiles_ko(Geometry g, 
             }
     } else {
         for (int t = lo; t < hi; ++t) {
-            const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
+            const int a = __ldg(toff + (int64_t)col * ntiles + t);
             csum += a;
-            psum += __ldg(toff + (int64_t)t * (ncol + 1) + col + 1) - a;
+            psum += __ldg(toff + (int64_t)(col + 1) * ntiles + t) - a;
         }
     }
     int x = psum, cx = csum;
@@ -1268,10 +1274,10 @@ __global__ void __launch_bounds__(kZThreads, ZKO_MINB) k_z_tiles_ko(Geometry g, 
         int32_t* pre = reinterpret_cast<int32_t*>(zsm + TLc.tables);
         int32_t* srca = pre + ntiles + 1;
         for (int t = lo; t < hi; ++t) {
-            const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
+            const int a = __ldg(toff + (int64_t)col * ntiles + t);
             srca[t] = t * tile + a;
             pre[t] = run;
-            run += __ldg(toff + (int64_t)t * (ncol + 1) + col + 1) - a;
+            run += __ldg(toff + (int64_t)(col + 1) * ntiles + t) - a;
         }
         if (tid == 0) pre[ntiles] = m;
         __syncthreads();
@@ -1297,8 +1303,8 @@ __global__ void __launch_bounds__(kZThreads, ZKO_MINB) k_z_tiles_ko(Geometry g, 
             }
     } else {
         for (int t = lo; t < hi; ++t) {
-            const int a = __ldg(toff + (int64_t)t * (ncol + 1) + col);
-            const int c = __ldg(toff + (int64_t)t * (ncol + 1) + col + 1) - a;
+            const int a = __ldg(toff + (int64_t)col * ntiles + t);
+            const int c = __ldg(toff + (int64_t)(col + 1) * ntiles + t) - a;
             const int64_t src0 = (int64_t)t * tile + a;
             for (int k = 0; k < c; ++k) cp_async8_s(s_pair + run + k, pairs + src0 + k);
             run += c;

@@ -30,6 +30,7 @@ __device__ __forceinline__ void put(int k, int slot, unsigned long long v) {
 #define TRACE_ACC(acc, a, b) acc += (b) - (a)
 #define TRACE_DECL(acc) long long acc = 0
 #define TRACE_PUT(k, slot, v) kb_trace_ns::put(k, slot, (unsigned long long)(v))
+#define TRACE_PTR(acc) (&acc)
 #define TRACE_READER(unit)                                                                              \
     extern "C" __attribute__((visibility("default"))) int kpme_debug_trace_##unit(int k,               \
                                                                                   unsigned long long* out) { \
@@ -42,5 +43,6 @@ __device__ __forceinline__ void put(int k, int slot, unsigned long long v) {
 #define TRACE_ACC(acc, a, b)
 #define TRACE_DECL(acc)
 #define TRACE_PUT(k, slot, v)
+#define TRACE_PTR(acc) nullptr
 #define TRACE_READER(unit)
 #endif

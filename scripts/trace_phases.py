@@ -47,8 +47,8 @@ for unit, k, desc in KERNELS:
     if os.environ.get("TRACE_DUMP"):
         print("  raw slots 4..6 of the first CTAs:", t[:3, 4:7].tolist())
     if unit == "interp" and k == 1 and (t[:, 7] > 10**12).all():
-        print("  gather prologue: tables loaded at %.2f us, x expansion done at %.2f us (CTA-relative means)" % (
-            ((t[:, 7] - t[:, 0]) / 1e3).mean(), ((t[:, 8] - t[:, 0]) / 1e3).mean()))
+        print("  gather prologue: tables loaded at %.2f us (CTA-relative mean); warp 0 cycles inside the Horner loops: mean %.0f" % (
+            ((t[:, 7] - t[:, 0]) / 1e3).mean(), t[:, 8].mean()))
     if unit == "interp" and k == 1 and (t[:, 5] > 0).all() and (t[:, 5] < 10**9).all():
         # cell-chunk gather, warp 0: cycles waiting for records / evaluating, Horner rounds
         print("  warp 0: wait cycles mean %.0f, work cycles mean %.0f, rounds mean %.1f -> %.0f cycles per round" % (

@@ -169,6 +169,8 @@ __global__ void k_core_c(Geometry g, const double* __restrict__ G, const double*
 __global__ void k_core_sum(int nblocks, int E, const double* __restrict__ Fpart,
                            double* __restrict__ F) {
     const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    pdl_trigger();  // the gather may become resident and load its tables
+    pdl_wait();     // the spread's partial cores
     if (e >= E) return;
     const double* row = Fpart + (int64_t)e * nblocks;
     // lane sums blocks lane + 64k (s0) and lane + 32 + 64k (s1) in increasing
@@ -293,7 +295,7 @@ void launch_core_backward(const Geometry& g, const double* G, const double* F, d
 void launch_core_sum(const Geometry& g, int nblocks, const double* Fpart, double* F,
                      cudaStream_t s) {
     const int E = g.R * g.R * g.R + 1;
-    k_core_sum<<<(E + 7) / 8, 256, 0, s>>>(nblocks, E, Fpart, F);
+    launch_pdl(k_core_sum, dim3((E + 7) / 8), dim3(256), 0, s, nblocks, E, Fpart, F);
     KB_CHECK_LAUNCH();
 }
 

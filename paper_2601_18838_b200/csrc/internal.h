@@ -52,6 +52,38 @@ inline void once_per_device(PerDevice& pd, F&& f) {
 // SM count of the current device (cached per device, thread-safe).
 int sm_count();
 
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may
+// start while its predecessor in the stream is still running, once every CTA
+// of the predecessor has executed pdl_trigger() (or exited); it must call
+// pdl_wait() before touching anything the predecessor writes. The column
+// kernels use it so that a kernel's CTAs are resident, and its table loads
+// done, when the grid-wide dependency (the summed core) arrives. Both device
+// calls are no-ops in a kernel launched the ordinary way. KPME_PDL=0 launches
+// everything the ordinary way.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("KPME_PDL");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    KB_CUDA(cudaLaunchKernelEx(&cfg, kern, KArgs(args)...));
+}
+
 // Makes `device` current for one ABI call and restores the caller's current
 // device afterwards (the reference API has no device state to disturb).
 struct DeviceGuard {

@@ -1085,6 +1085,7 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
     const ColumnRange cr = column_range(g, a.S);
     extern __shared__ double sm[];
     TRACE_MARK(0, 0);
+    pdl_trigger();  // the core sum's CTAs may take the slots this kernel's CTAs free
     const int per_warp = spread_f8_warp_doubles<L>(R);
     double* St = sm + warp * per_warp;  // [32][SR] staged particle rows
     double* ph = St + M::stage;         // [MT2*8][LDK] finished cell grid
@@ -1882,9 +1883,8 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
     auto stage_xy = [&](int st) { return reinterpret_cast<double2*>(st ? scr : ring0) + warp * kCcChunk; };
     auto stage_z = [&](int st) { return (st ? scr : ring0) + NW * kCcChunk * 2 + warp * kCcChunk; };
     const CellAxis ax0 = cell_axis_tab(a.cellax[0], cr.c0), ax1 = cell_axis_tab(a.cellax[1], cr.c1);
-    double corr = a.corr ? *a.corr : 0.0;
     const bool fused = a.B2 == nullptr;
-    if (fused) corr = 0.0;
+    double corr = 0.0;  // fused: the zero mode carries the correction; else read after pdl_wait()
     double tmax = 0.0;
     for (int cb0 = cr.zb; cb0 < cr.ze; cb0 += cells_per_batch) {
         const bool first = cb0 == cr.zb;
@@ -1906,18 +1906,11 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
             const int st0 = tid <= nb ? __ldg(a.start + cell0 + tid) : 0;
             double4 axv = make_double4(0.0, 0.0, 0.0, 0.0);
             if (tid < nb) axv = a.cellax[2][cb0 + tid];
-            double fq = 0.0;  // sum q (the last core entry), for the zero mode
             if (first && fused) {
-                if (tid == 0) fq = __ldg(a.Fc + R3);
                 if (h_regs) {
 #pragma unroll
-                    for (int u = 0; u < HU; ++u) {
-                        const int e = tid + NTH * u;
-                        if (e < R3) {
-                            gv[u] = __ldg(a.Gc + e);
-                            fv[u] = __ldg(a.Fc + e);
-                        }
-                    }
+                    for (int u = 0; u < HU; ++u)
+                        if (tid + NTH * u < R3) gv[u] = __ldg(a.Gc + tid + NTH * u);
                 }
                 if (tid < R * L) {
                     wa = a.W0[(int64_t)(tid / L) * g.n[0] + cr.c0 * L + tid % L];
@@ -1937,15 +1930,23 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
                     w2s[e] = __ldg(a.W2 + (int64_t)(e / nz) * g.n[2] + cb0 * L + e % nz);
             }
             if (first && fused) {
+                // Everything above is independent of the summed core: under a
+                // programmatic dependent launch it ran while the core sum did.
+                pdl_wait();
+                double fq = 0.0;  // sum q (the last core entry), for the zero mode
+                if (tid == 0) fq = __ldcg(a.Fc + R3);
                 // zero mode, exactly: h[0] = (G[0] - c) sum q
                 if (h_regs) {
+#pragma unroll
+                    for (int u = 0; u < HU; ++u)
+                        if (tid + NTH * u < R3) fv[u] = __ldcg(a.Fc + tid + NTH * u);
 #pragma unroll
                     for (int u = 0; u < HU; ++u)
                         if (tid + NTH * u < R3)
                             h[tid + NTH * u] = (u == 0 && tid == 0) ? (gv[0] - a.correction) * fq : gv[u] * fv[u];
                 } else {
                     for (int e = tid; e < R3; e += NTH)
-                        h[e] = e == 0 ? (__ldg(a.Gc) - a.correction) * fq : __ldg(a.Gc + e) * __ldg(a.Fc + e);
+                        h[e] = e == 0 ? (__ldg(a.Gc) - a.correction) * fq : __ldg(a.Gc + e) * __ldcg(a.Fc + e);
                 }
                 if (tid < R * L) {
                     w01[tid] = wa;
@@ -1956,6 +1957,8 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
                     w01[R * L + e] = a.W1[(int64_t)(e / L) * g.n[1] + cr.c1 * L + e % L];
                 }
             } else if (first) {
+                pdl_wait();
+                corr = a.corr ? *a.corr : 0.0;
                 for (int e = tid; e < L2 * R; e += NTH) {
                     const int ij = e / R, r = e % R, i = ij / L, j = ij % L;
                     b2s[e] = a.B2[((int64_t)(cr.c0 * L + i) * g.n[1] + cr.c1 * L + j) * R + r];
@@ -2328,13 +2331,13 @@ void launch_gather_t(const ColumnArgs& a0, int mode, cudaStream_t s) {
                 });
                 const bool waves = grid > 2 * 3 * sm_count() && csm * 4 <= 220 * 1024;
                 if (R == 9 && waves)
-                    k_gather_cc<L, 4, 9><<<grid, 128, csm, s>>>(a, ccb);
+                    launch_pdl(k_gather_cc<L, 4, 9>, dim3(grid), dim3(128), csm, s, a, ccb);
                 else if (R == 9)
-                    k_gather_cc<L, 3, 9><<<grid, 128, csm, s>>>(a, ccb);
+                    launch_pdl(k_gather_cc<L, 3, 9>, dim3(grid), dim3(128), csm, s, a, ccb);
                 else if (waves)
-                    k_gather_cc<L, 4, 0><<<grid, 128, csm, s>>>(a, ccb);
+                    launch_pdl(k_gather_cc<L, 4, 0>, dim3(grid), dim3(128), csm, s, a, ccb);
                 else
-                    k_gather_cc<L, 3, 0><<<grid, 128, csm, s>>>(a, ccb);
+                    launch_pdl(k_gather_cc<L, 3, 0>, dim3(grid), dim3(128), csm, s, a, ccb);
                 KB_CHECK_LAUNCH();
                 return;
             }

@@ -1086,6 +1086,7 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
     extern __shared__ double sm[];
     TRACE_MARK(0, 0);
     pdl_trigger();  // the core sum's CTAs may take the slots this kernel's CTAs free
+    pdl_wait();     // the sort's cell starts and records
     const int per_warp = spread_f8_warp_doubles<L>(R);
     double* St = sm + warp * per_warp;  // [32][SR] staged particle rows
     double* ph = St + M::stage;         // [MT2*8][LDK] finished cell grid
@@ -2224,15 +2225,15 @@ bool launch_spread_f8_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
         const bool waves = grid > 2 * 3 * sm_count() && smem * 4 <= 220 * 1024;
         // n-tiles of the W2 contraction over r = 1 .. R-1
         if (a.g.R <= 9 && waves)
-            k_spread_f8<L, 1, 4><<<grid, 32 * F8_NW, smem, s>>>(a, want_fwd ? 1 : 0);
+            launch_pdl(k_spread_f8<L, 1, 4>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
         else if (a.g.R <= 9)
-            k_spread_f8<L, 1, 3><<<grid, 32 * F8_NW, smem, s>>>(a, want_fwd ? 1 : 0);
+            launch_pdl(k_spread_f8<L, 1, 3>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
         else if (a.g.R <= 17 && waves)
-            k_spread_f8<L, 2, 4><<<grid, 32 * F8_NW, smem, s>>>(a, want_fwd ? 1 : 0);
+            launch_pdl(k_spread_f8<L, 2, 4>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
         else if (a.g.R <= 17)
-            k_spread_f8<L, 2, 3><<<grid, 32 * F8_NW, smem, s>>>(a, want_fwd ? 1 : 0);
+            launch_pdl(k_spread_f8<L, 2, 3>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
         else
-            k_spread_f8<L, 4, 3><<<grid, 32 * F8_NW, smem, s>>>(a, want_fwd ? 1 : 0);
+            launch_pdl(k_spread_f8<L, 4, 3>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
         KB_CHECK_LAUNCH();
         return true;
     } else {

@@ -1101,6 +1101,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, KEYS_MINB) k_tile_keys(Geomet
     int32_t* cb = reinterpret_cast<int32_t*>(tsm + TL.cb);
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
     TRACE_MARK(0, 0);
+    pdl_trigger();  // the column pass may become resident
     for (int e = tid; e < (int)((TL.tc - TL.wc) / 16); e += blockDim.x)
         reinterpret_cast<uint4*>(wc)[e] = make_uint4(0u, 0u, 0u, 0u);
     const int64_t tbase = (int64_t)blockIdx.x * kTT;
@@ -1229,6 +1230,8 @@ __global__ void __launch_bounds__(kZThreads, ZKO_MINB) k_z_tiles_ko(Geometry g, 
     const int per = (ntiles + kZThreads - 1) / kZThreads;
     const int lo = min(ntiles, tid * per), hi = min(ntiles, lo + per);
     TRACE_MARK(1, 0);
+    pdl_trigger();  // the spread may become resident
+    pdl_wait();     // the tile pass's offsets and pairs
     int a_[4], e_[4];
     int csum = 0, psum = 0;
     if (per <= 4) {
@@ -1458,8 +1461,8 @@ static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, 
 #ifdef ZKO_NOSP  // profiling ablation only: no record write-out (results invalid)
         sp = nullptr;
 #endif
-        zk<<<ncol, kZThreads, kzsmem, s>>>(g, n, ntiles, tile, pcap, b.hist, pairs, xyz, q, b.perm, b.start,
-                                           sp);
+        launch_pdl(zk, dim3(ncol), dim3(kZThreads), kzsmem, s, g, n, ntiles, tile, pcap, b.hist, pairs, xyz, q,
+                   b.perm, b.start, sp);
         KB_CHECK_LAUNCH();
         if (launches) *launches += l + 1;
         return true;

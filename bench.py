@@ -356,7 +356,7 @@ def stage_rooflines(torch, plan, run_eager, w, n, K, flush, steps, peaks, fp64):
             r = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                  "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
         if name == "k_sort_stage":
-            r["kernels"] = "k_tile_sort + k_z_tiles (<= 512 columns) or k_tile_hist + k_col_scan + k_col_scatter + k_z_sort"
+            r["kernels"] = "k_tile_keys + k_z_tiles_ko (key path, <= 512 columns) or k_tile_hist + k_col_scan + k_col_scatter + k_z_sort"
         r.update({"kernel": name, "algorithmic_flops": flops, "algorithmic_bytes": bytes_,
                   "kernel_ms": t_ms, "traffic": ncu_traffic(name),
                   "traffic_source": "profiles/ncu_summary.json (ncu --set full of this workload)"})

@@ -526,6 +526,93 @@ __device__ __forceinline__ void spread_epilogue(const ColumnArgs& a, const Colum
     }
 }
 
+// The fused epilogue for the common R = 2M + 1 = RC (RC = 9 at M = 4), with
+// compile-time index arithmetic, every thread's outputs of a phase in flight
+// together, the column's W0 / W1 rows already in shared memory (w01, loaded by
+// spread_epilogue_tables at kernel start) and a shuffle tree for sum q.
+template <int L>
+__device__ __forceinline__ void spread_epilogue_tables(const ColumnArgs& a, const ColumnRange& cr, double* epi,
+                                                       int nthreads) {
+    const Geometry& g = a.g;
+    const int R = g.R;
+    double* w01 = epi + L * L * R + L * R * R;  // [2][R][L]
+    if (a.Fpart)
+        for (int e = threadIdx.x; e < R * L; e += nthreads) {
+            w01[e] = a.W0[(int64_t)(e / L) * g.n[0] + cr.c0 * L + e % L];
+            w01[R * L + e] = a.W1[(int64_t)(e / L) * g.n[1] + cr.c1 * L + e % L];
+        }
+}
+template <int L, int NW, int RC>
+__device__ __forceinline__ void spread_epilogue_rc(const ColumnArgs& a, const ColumnRange& cr, double* sm,
+                                                   int per_warp, int t1off, int RP, double* epi,
+                                                   double* red, double qsum) {
+    constexpr int L2 = L * L, NTH = 32 * NW, RR = RC * RC;
+    const Geometry& g = a.g;
+    const int tid = threadIdx.x;
+    double* tc = epi;                // [L^2][RC]
+    double* u = tc + L2 * RC;        // [L][RC][RC]
+    const double* w01 = u + L * RR;  // [2][RC][L]
+    double qs = qsum;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qs += __shfl_xor_sync(0xffffffffu, qs, o);
+    __syncthreads();  // every warp's T1 partial is in shared memory
+    if ((tid & 31) == 0) red[tid >> 5] = qs;
+    {
+        constexpr int N = L2 * RC, IT = (N + NTH - 1) / NTH;
+        double sv[IT];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int e = min(tid + it * NTH, N - 1), ij = e / RC, r = e % RC;
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) s += sm[w * per_warp + t1off + ij * RP + r];
+            sv[it] = s;
+        }
+#pragma unroll
+        for (int it = 0; it < IT; ++it)
+            if (tid + it * NTH < N) tc[tid + it * NTH] = sv[it];
+    }
+    __syncthreads();
+    {
+        constexpr int N = L * RR, IT = (N + NTH - 1) / NTH;
+        double sv[IT];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int e = min(tid + it * NTH, N - 1), i = e / RR, r1 = (e / RC) % RC, r2 = e % RC;
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < L; ++j) s = fma(w01[RC * L + r1 * L + j], tc[(i * L + j) * RC + r2], s);
+            sv[it] = s;
+        }
+#pragma unroll
+        for (int it = 0; it < IT; ++it)
+            if (tid + it * NTH < N) u[tid + it * NTH] = sv[it];
+    }
+    __syncthreads();
+    const int nblocks = a.fstride > 0 ? a.fstride : a.S * g.K[0] * g.K[1];
+    double* dst = a.Fpart + (int64_t)cr.seg * g.K[0] * g.K[1] + cr.col;
+    {
+        constexpr int N = RR * RC, IT = (N + NTH - 1) / NTH;
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int e = tid + it * NTH;
+            if (e < N) {
+                const int r0 = e / RR, rr = e % RR;
+                double s = 0.0;
+#pragma unroll
+                for (int i = 0; i < L; ++i) s = fma(w01[r0 * L + i], u[i * RR + rr], s);
+                dst[(int64_t)e * nblocks] = s;
+            }
+        }
+    }
+    if (tid == 0) {
+        double q = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) q += red[w];
+        dst[(int64_t)RR * RC * nblocks] = q;
+    }
+}
+
 template <int L, bool MONO>
 __global__ void __launch_bounds__(128, SPREAD_MINB) k_spread_mma(ColumnArgs a, int want_fwd) {
     using T = SpreadTile<L>;
@@ -1096,6 +1183,7 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
     double* epi = sm + NW * per_warp;   // epilogue scratch
     __shared__ double red[NTH];
     __shared__ int cst[66];
+    spread_epilogue_tables<L>(a, cr, epi, NTH);  // W0 / W1 column rows, used after the particles
     for (int e = lane; e < M::ph; e += 32) ph[e] = 0.0;  // padding stays zero
     const int col_cell0 = (cr.c0 * g.K[1] + cr.c1) * g.K[2];
     const int nz = cr.ze - cr.zb;
@@ -1333,7 +1421,10 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
         if (a.Fpart && sm[threadIdx.x] + qsum == 1.2345) a.Fpart[0] = 0.0;
         return;
     }
-    spread_epilogue<L, NW>(a, cr, sm, per_warp, t1off, RP, epi, red, qsum, want_fwd);
+    if (want_fwd && a.Fpart && R == 9)
+        spread_epilogue_rc<L, NW, 9>(a, cr, sm, per_warp, t1off, RP, epi, red, qsum);
+    else
+        spread_epilogue<L, NW>(a, cr, sm, per_warp, t1off, RP, epi, red, qsum, want_fwd);
     TRACE_MARK(0, 3);
 }
 

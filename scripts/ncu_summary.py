@@ -13,7 +13,8 @@ rep, out, desc = sys.argv[1], sys.argv[2], sys.argv[3]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, data = rows[0], rows[2:]
-KEYS = [("k_spread_f8", "k_spread_fwd"), ("k_spread_uv", "k_spread_fwd"), ("k_dgemm_tn_tma", "k_dgemm_tn"),
+KEYS = [("k_gather_cc", "k_bwd_gather"), ("k_tile_keys", "k_tile_keys"), ("k_z_tiles_ko", "k_z_tiles_ko"),
+        ("k_spread_f8", "k_spread_fwd"), ("k_spread_uv", "k_spread_fwd"), ("k_dgemm_tn_tma", "k_dgemm_tn"),
         ("k_dgemm_tn", "k_dgemm_tn"), ("k_spread_mma", "k_spread_fwd"), ("k_bwd_gather", "k_bwd_gather"),
         ("k_col_scatter", "k_col_scatter"), ("k_z_sort", "k_z_sort"), ("k_tile_hist", "k_tile_hist"),
         ("k_col_scan", "k_col_scan"), ("k_tile_sort", "k_tile_sort"), ("k_z_tiles", "k_z_tiles"),

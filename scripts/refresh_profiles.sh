@@ -15,7 +15,7 @@ python scripts/profile_step.py cfg3 3 > /dev/null 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_step.csv \
     python scripts/profile_step.py cfg3 3 > gpurun_out/ncu_launch_step.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_spread|k_bwd_gather|k_col_scatter|k_z_sort|k_tile_hist|k_col_scan|k_tile_sort|k_z_tiles|k_core_sum" -c 5 \
+    -k regex:"k_spread|k_bwd_gather|k_gather_cc|k_col_scatter|k_z_sort|k_tile_hist|k_col_scan|k_tile_sort|k_tile_keys|k_z_tiles|k_core_sum" -c 5 \
     -f -o gpurun_out/full python scripts/profile_step.py cfg3 1 > gpurun_out/ncu_full.log 2>&1
 tail -1 gpurun_out/ncu_full.log
 python scripts/dense_once.py 256 16 > /dev/null 2>&1 || exit 1

@@ -545,13 +545,14 @@ __device__ __forceinline__ void spread_epilogue_tables(const ColumnArgs& a, cons
 template <int L, int NW, int RC>
 __device__ __forceinline__ void spread_epilogue_rc(const ColumnArgs& a, const ColumnRange& cr, double* sm,
                                                    int per_warp, int t1off, int RP, double* epi,
-                                                   double* red, double qsum) {
+                                                   double* red, double qsum,
+                                                   const double* w01_at = nullptr) {
     constexpr int L2 = L * L, NTH = 32 * NW, RR = RC * RC;
     const Geometry& g = a.g;
     const int tid = threadIdx.x;
     double* tc = epi;                // [L^2][RC]
     double* u = tc + L2 * RC;        // [L][RC][RC]
-    const double* w01 = u + L * RR;  // [2][RC][L]
+    const double* w01 = w01_at ? w01_at : u + L * RR;  // [2][RC][L]
     double qs = qsum;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) qs += __shfl_xor_sync(0xffffffffu, qs, o);
@@ -1274,6 +1275,10 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
     TRACE_MARK(0, 1);
 #pragma unroll
     for (int u = 0; u < M::RING - 1; ++u) issue();
+    TRACE_DECL(tr_wait);
+    TRACE_DECL(tr_stage);
+    TRACE_DECL(tr_kloop);
+    TRACE_DECL(tr_drain);
     for (int c2 = zw0; c2 < zw1; ++c2) {
         const int s0 = cell_lo_p(c2), s1 = cell_hi_p(c2);
         if (s0 >= s1) {
@@ -1288,8 +1293,10 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
         for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
         for (int base = s0; base < s1; base += 32) {
             const int cnt = min(32, s1 - base);
+            TRACE_CLK(c0);
             issue();
             cp_async_wait<M::RING - 1>();
+            TRACE_CLK(c1);
             const double4 pt = ring[cslot * 32 + lane];
             cslot = cslot + 1 == M::RING ? 0 : cslot + 1;
             const double q = lane < cnt ? pt.w : 0.0;
@@ -1334,6 +1341,7 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
                 *reinterpret_cast<double2*>(row + 14) = make_double2(qab * c2v, t0 * b1c1);
             }
             __syncwarp();
+            TRACE_CLK(c2_);
             const int ks = (F8_SKIP & 1) ? 0 : (cnt + 3) >> 2;
             for (int kk = 0; kk < ks; ++kk) {
                 const double* r = St + (kk * 4 + tg) * SR;
@@ -1350,7 +1358,12 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
                     dmma884(acc[0], au.x, au.y);
                 }
             }
+            TRACE_CLK(c3);
+            TRACE_ACC(tr_wait, c0, c1);
+            TRACE_ACC(tr_stage, c1, c2_);
+            TRACE_ACC(tr_kloop, c2_, c3);
         }
+        TRACE_CLK(d0);
         __syncwarp();
         if (F8_SKIP & 2) {
             t1acc[0][0][0] += acc[0][0] + acc[NT - 1][1] + St[lane];
@@ -1393,7 +1406,13 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
                 }
         }
         __syncwarp();
+        TRACE_CLK(d1);
+        TRACE_ACC(tr_drain, d0, d1);
     }
+    TRACE_PUT(0, 4, tr_wait);
+    TRACE_PUT(0, 5, tr_stage);
+    TRACE_PUT(0, 6, tr_kloop);
+    TRACE_PUT(0, 7, tr_drain);
     cp_async_wait<0>();
     __syncwarp();
     TRACE_MARK(0, 2);

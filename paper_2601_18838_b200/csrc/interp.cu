@@ -1204,7 +1204,19 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
 #pragma unroll
         for (int t = 0; t < RTM; ++t) t1acc[mt][t][0] = t1acc[mt][t][1] = 0.0;
     __syncthreads();
-    auto cstart = [&](int c2) { return cst_ok ? cst[c2 - cr.zb] : a.start[col_cell0 + c2]; };
+    // the column's cell starts: explicit shared-memory loads (through the lambdas
+    // the table would be read with generic loads and a window-address rebuild)
+    const unsigned cst_sa = (unsigned)__cvta_generic_to_shared(cst);
+    const int zb0 = cr.zb;
+    const int32_t* gstart = a.start + col_cell0;
+    auto cstart = [=](int c2) {
+        int v;
+        if (cst_ok)
+            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(cst_sa + 4u * (unsigned)(c2 - zb0)));
+        else
+            v = gstart[c2];
+        return v;
+    };
 
     // Warp w takes particles [pw0, pw1), an exact quarter of the column segment
     // (cells shared by two warps add linearly); whole cells for phi_cells.
@@ -1235,20 +1247,24 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
     // record: finite t, q masked to 0 below).
     auto cell_lo_p = [&](int c) { return max(cstart(c), pw0); };
     auto cell_hi_p = [&](int c) { return min(cstart(c + 1), pw1); };
-    int nc2 = zw0, nbase = zw0 < zw1 ? cell_lo_p(zw0) : 0;
-    auto norm = [&]() {
-        while (nc2 < zw1 && nbase >= cell_hi_p(nc2)) {
+    // producer cursor: cell nc2, next record nbase, the cell's end nhi (the
+    // table is read only when the cursor enters a cell; empty cells are skipped)
+    int nc2 = zw0, nbase = 0, nhi = 0;
+    auto enter_cell = [&]() {
+        while (nc2 < zw1) {
+            nbase = cell_lo_p(nc2);
+            nhi = cell_hi_p(nc2);
+            if (nbase < nhi) break;
             ++nc2;
-            if (nc2 < zw1) nbase = cell_lo_p(nc2);
         }
     };
-    norm();
+    enter_cell();
     int pslot = 0, cslot = 0;
     // direct records: the particle index of the chunk to be issued is loaded
     // one chunk earlier (pidx), so the copies never wait on the perm load
     int pidx = 0;
     auto perm_at = [&]() {
-        return nc2 < zw1 ? __ldg(a.perm + min(nbase + lane, cell_hi_p(nc2) - 1)) : 0;
+        return nc2 < zw1 ? __ldg(a.perm + min(nbase + lane, nhi - 1)) : 0;
     };
     if (a.direct) pidx = perm_at();
     auto issue = [&]() {
@@ -1261,12 +1277,15 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
                 cp_async8_sm(reinterpret_cast<char*>(dst) + 16, src + 2);
                 cp_async8_sm(reinterpret_cast<char*>(dst) + 24, a.qv + pidx);
             } else {
-                const double4* src = a.sp + min(nbase + lane, cell_hi_p(nc2) - 1);
+                const double4* src = a.sp + min(nbase + lane, nhi - 1);
                 cp_async16_sm(dst, src);
                 cp_async16_sm(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(src) + 16);
             }
             nbase += 32;
-            norm();
+            if (nbase >= nhi) {
+                ++nc2;
+                enter_cell();
+            }
             if (a.direct) pidx = perm_at();
         }
         cp_async_commit();
@@ -1276,6 +1295,7 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
 #pragma unroll
     for (int u = 0; u < M::RING - 1; ++u) issue();
     TRACE_DECL(tr_wait);
+    TRACE_DECL(tr_issue);
     TRACE_DECL(tr_stage);
     TRACE_DECL(tr_kloop);
     TRACE_DECL(tr_drain);
@@ -1295,8 +1315,10 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
             const int cnt = min(32, s1 - base);
             TRACE_CLK(c0);
             issue();
+            TRACE_CLK(c0b);
             cp_async_wait<M::RING - 1>();
             TRACE_CLK(c1);
+            TRACE_ACC(tr_issue, c0, c0b);
             const double4 pt = ring[cslot * 32 + lane];
             cslot = cslot + 1 == M::RING ? 0 : cslot + 1;
             const double q = lane < cnt ? pt.w : 0.0;
@@ -1315,14 +1337,19 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
                 const double qT1 = q * T1, qT0 = q * T0, qT0T1 = qT0 * T1;
                 const double b1c1 = t1 * t2, b1c2 = t1 * c2v, b2c1 = b2 * t2, b2c2 = b2 * c2v;
                 // [A_g, U_g] pairs, g = (ih, jh, kh) for A and 3 jl + kl for U
-                *reinterpret_cast<double2*>(row + 0) = make_double2(q, 1.0);
-                *reinterpret_cast<double2*>(row + 2) = make_double2(q * T2, t2);
-                *reinterpret_cast<double2*>(row + 4) = make_double2(qT1, c2v);
-                *reinterpret_cast<double2*>(row + 6) = make_double2(qT1 * T2, t1);
-                *reinterpret_cast<double2*>(row + 8) = make_double2(qT0, b1c1);
-                *reinterpret_cast<double2*>(row + 10) = make_double2(qT0 * T2, b1c2);
-                *reinterpret_cast<double2*>(row + 12) = make_double2(qT0T1, b2);
-                *reinterpret_cast<double2*>(row + 14) = make_double2(qT0T1 * T2, b2c1);
+                // pair g of row l sits at pair slot (g + ((l >> 2) & 1)) & 7: with the 160-byte
+                // row stride, lanes l and l + 4 of a quarter-warp then store to different banks
+                // (conflict-free 128-bit stores); a k-step reads rows 4 kk + tg, so its
+                // rotation kk & 1 is warp-uniform and the reads stay conflict-free
+                const int sh = (lane >> 2) & 1;
+                *reinterpret_cast<double2*>(row + 2 * ((0 + sh) & 7)) = make_double2(q, 1.0);
+                *reinterpret_cast<double2*>(row + 2 * ((1 + sh) & 7)) = make_double2(q * T2, t2);
+                *reinterpret_cast<double2*>(row + 2 * ((2 + sh) & 7)) = make_double2(qT1, c2v);
+                *reinterpret_cast<double2*>(row + 2 * ((3 + sh) & 7)) = make_double2(qT1 * T2, t1);
+                *reinterpret_cast<double2*>(row + 2 * ((4 + sh) & 7)) = make_double2(qT0, b1c1);
+                *reinterpret_cast<double2*>(row + 2 * ((5 + sh) & 7)) = make_double2(qT0 * T2, b1c2);
+                *reinterpret_cast<double2*>(row + 2 * ((6 + sh) & 7)) = make_double2(qT0T1, b2);
+                *reinterpret_cast<double2*>(row + 2 * ((7 + sh) & 7)) = make_double2(qT0T1 * T2, b2c1);
                 // [t0, W0, W1, W2] with W_g = t0^g t1^2 t2^2
                 *reinterpret_cast<double2*>(row + 16) = make_double2(t0, b2c2);
                 *reinterpret_cast<double2*>(row + 18) = make_double2(b2c2 * t0, b2c2 * a2);
@@ -1331,21 +1358,22 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
                 const double a2 = t0 * t0, b2 = t1 * t1, c2v = t2 * t2;
                 const double qb = q * b2, qa = q * a2, qab = qa * b2;
                 const double b1c1 = t1 * t2;
-                *reinterpret_cast<double2*>(row + 0) = make_double2(q, 1.0);
-                *reinterpret_cast<double2*>(row + 2) = make_double2(q * c2v, t2);
-                *reinterpret_cast<double2*>(row + 4) = make_double2(qb, t1);
-                *reinterpret_cast<double2*>(row + 6) = make_double2(qb * c2v, b1c1);
-                *reinterpret_cast<double2*>(row + 8) = make_double2(qa, t0);
-                *reinterpret_cast<double2*>(row + 10) = make_double2(qa * c2v, t0 * t2);
-                *reinterpret_cast<double2*>(row + 12) = make_double2(qab, t0 * t1);
-                *reinterpret_cast<double2*>(row + 14) = make_double2(qab * c2v, t0 * b1c1);
+                const int sh = (lane >> 2) & 1;  // see L = 6
+                *reinterpret_cast<double2*>(row + 2 * ((0 + sh) & 7)) = make_double2(q, 1.0);
+                *reinterpret_cast<double2*>(row + 2 * ((1 + sh) & 7)) = make_double2(q * c2v, t2);
+                *reinterpret_cast<double2*>(row + 2 * ((2 + sh) & 7)) = make_double2(qb, t1);
+                *reinterpret_cast<double2*>(row + 2 * ((3 + sh) & 7)) = make_double2(qb * c2v, b1c1);
+                *reinterpret_cast<double2*>(row + 2 * ((4 + sh) & 7)) = make_double2(qa, t0);
+                *reinterpret_cast<double2*>(row + 2 * ((5 + sh) & 7)) = make_double2(qa * c2v, t0 * t2);
+                *reinterpret_cast<double2*>(row + 2 * ((6 + sh) & 7)) = make_double2(qab, t0 * t1);
+                *reinterpret_cast<double2*>(row + 2 * ((7 + sh) & 7)) = make_double2(qab * c2v, t0 * b1c1);
             }
             __syncwarp();
             TRACE_CLK(c2_);
             const int ks = (F8_SKIP & 1) ? 0 : (cnt + 3) >> 2;
             for (int kk = 0; kk < ks; ++kk) {
                 const double* r = St + (kk * 4 + tg) * SR;
-                const double2 au = *reinterpret_cast<const double2*>(r + 2 * gg);
+                const double2 au = *reinterpret_cast<const double2*>(r + 2 * ((gg + (kk & 1)) & 7));
                 if (L == 6) {
                     const double tt = r[16];
                     const double w = gg < 3 ? r[17 + gg] : 0.0;
@@ -1410,6 +1438,7 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
         TRACE_ACC(tr_drain, d0, d1);
     }
     TRACE_PUT(0, 4, tr_wait);
+    TRACE_PUT(0, 8, tr_issue);
     TRACE_PUT(0, 5, tr_stage);
     TRACE_PUT(0, 6, tr_kloop);
     TRACE_PUT(0, 7, tr_drain);

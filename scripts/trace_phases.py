@@ -47,8 +47,8 @@ for unit, k, desc in KERNELS:
     if os.environ.get("TRACE_DUMP"):
         print("  raw slots 4..6 of the first CTAs:", t[:3, 4:7].tolist())
     if unit == "interp" and k == 0 and (t[:, 6] > 0).all() and (t[:, 6] < 10**9).all():
-        print("  spread warp 0 cycles: record wait %.0f, staging %.0f, k-steps %.0f, per-cell drain + contraction %.0f" % (
-            t[:, 4].mean(), t[:, 5].mean(), t[:, 6].mean(), t[:, 7].mean()))
+        print("  spread warp 0 cycles: record issue + wait %.0f (issue alone %.0f), staging %.0f, k-steps %.0f, per-cell drain + contraction %.0f" % (
+            t[:, 4].mean(), t[:, 8].mean(), t[:, 5].mean(), t[:, 6].mean(), t[:, 7].mean()))
     if unit == "interp" and k == 1 and (t[:, 7] > 10**12).all():
         print("  gather prologue: tables loaded at %.2f us (CTA-relative mean); warp 0 cycles inside the Horner loops: mean %.0f" % (
             ((t[:, 7] - t[:, 0]) / 1e3).mean(), t[:, 8].mean()))

@@ -1178,7 +1178,9 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
     const int per_warp = spread_f8_warp_doubles<L>(R);
     double* St = sm + warp * per_warp;  // [32][SR] staged particle rows
     double* ph = St + M::stage;         // [MT2*8][LDK] finished cell grid
-    double4* ring = reinterpret_cast<double4*>(ph + M::ph);  // [RING][32] records, lane-private
+    // [RING][2][32] records, lane-private: (x, y) of the 32 lanes, then (z, q): every 16-byte
+    // copy of a warp lands on 512 contiguous bytes (a double4 per lane is 8-way conflicted)
+    double2* ring = reinterpret_cast<double2*>(ph + M::ph);
     const int t1off = spread_f8_t1off<L>(R);
     double* t1w = St + t1off;           // [MT2*8][RP]  warp partial of T1 (after the chunks)
     double* epi = sm + NW * per_warp;   // epilogue scratch
@@ -1269,17 +1271,18 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
     if (a.direct) pidx = perm_at();
     auto issue = [&]() {
         if (nc2 < zw1) {
-            double4* dst = ring + pslot * 32 + lane;
+            double2* dlo = ring + pslot * 64 + lane;
+            double2* dhi = dlo + 32;
             if (a.direct) {
                 const double* src = a.xyz + 3 * (int64_t)pidx;
-                cp_async8_sm(dst, src);
-                cp_async8_sm(reinterpret_cast<char*>(dst) + 8, src + 1);
-                cp_async8_sm(reinterpret_cast<char*>(dst) + 16, src + 2);
-                cp_async8_sm(reinterpret_cast<char*>(dst) + 24, a.qv + pidx);
+                cp_async8_sm(dlo, src);
+                cp_async8_sm(reinterpret_cast<char*>(dlo) + 8, src + 1);
+                cp_async8_sm(dhi, src + 2);
+                cp_async8_sm(reinterpret_cast<char*>(dhi) + 8, a.qv + pidx);
             } else {
                 const double4* src = a.sp + min(nbase + lane, nhi - 1);
-                cp_async16_sm(dst, src);
-                cp_async16_sm(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(src) + 16);
+                cp_async16_sm(dlo, src);
+                cp_async16_sm(dhi, reinterpret_cast<const char*>(src) + 16);
             }
             nbase += 32;
             if (nbase >= nhi) {
@@ -1319,7 +1322,8 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
             cp_async_wait<M::RING - 1>();
             TRACE_CLK(c1);
             TRACE_ACC(tr_issue, c0, c0b);
-            const double4 pt = ring[cslot * 32 + lane];
+            const double2 pxy = ring[cslot * 64 + lane], pzq = ring[cslot * 64 + 32 + lane];
+            const double4 pt = make_double4(pxy.x, pxy.y, pzq.x, pzq.y);
             cslot = cslot + 1 == M::RING ? 0 : cslot + 1;
             const double q = lane < cnt ? pt.w : 0.0;
             qsum += q;
@@ -1350,9 +1354,9 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
                 *reinterpret_cast<double2*>(row + 2 * ((5 + sh) & 7)) = make_double2(qT0 * T2, b1c2);
                 *reinterpret_cast<double2*>(row + 2 * ((6 + sh) & 7)) = make_double2(qT0T1, b2);
                 *reinterpret_cast<double2*>(row + 2 * ((7 + sh) & 7)) = make_double2(qT0T1 * T2, b2c1);
-                // [t0, W0, W1, W2] with W_g = t0^g t1^2 t2^2
-                *reinterpret_cast<double2*>(row + 16) = make_double2(t0, b2c2);
-                *reinterpret_cast<double2*>(row + 18) = make_double2(b2c2 * t0, b2c2 * a2);
+                // [t0, W0, W1, W2] with W_g = t0^g t1^2 t2^2; the two pairs swap on rotated rows
+                *reinterpret_cast<double2*>(row + 16 + 2 * sh) = make_double2(t0, b2c2);
+                *reinterpret_cast<double2*>(row + 18 - 2 * sh) = make_double2(b2c2 * t0, b2c2 * a2);
             } else {
                 // L = 4: [A_g, B_g], A_g = q t0^(2ih) t1^(2jh) t2^(2kh), B_g = t0^il t1^jl t2^kl
                 const double a2 = t0 * t0, b2 = t1 * t1, c2v = t2 * t2;
@@ -1375,8 +1379,9 @@ __global__ void __launch_bounds__(32 * F8_NW, MINB) k_spread_f8(ColumnArgs a, in
                 const double* r = St + (kk * 4 + tg) * SR;
                 const double2 au = *reinterpret_cast<const double2*>(r + 2 * ((gg + (kk & 1)) & 7));
                 if (L == 6) {
-                    const double tt = r[16];
-                    const double w = gg < 3 ? r[17 + gg] : 0.0;
+                    const int s2 = 2 * (kk & 1);  // the row's rotation
+                    const double tt = r[16 + s2];
+                    const double w = gg < 3 ? r[16 + ((1 + gg + s2) & 3)] : 0.0;
                     const double b1 = au.y * tt;
                     dmma884(acc[0], au.x, au.y);
                     dmma884(acc[3], au.x, w);

@@ -2113,18 +2113,28 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
         __syncthreads();
         if (first) TRACE_MARK(1, 7);
         // The warp's particle range of this batch and its first chunk's records:
-        // requested now, they arrive while the expansions below run.
-        const int P0 = gcst[0], P1 = gcst[nb];
+        // requested now, they arrive while the expansions below run. (The cell
+        // starts are read with explicit shared loads: through the lambdas below
+        // the table would be read with generic loads and a window-address rebuild.)
+        const unsigned gcst_sa = (unsigned)__cvta_generic_to_shared(gcst);
+        auto gc = [=](int e) {
+            int v;
+            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(gcst_sa + 4u * (unsigned)e));
+            return v;
+        };
+        const int P0 = gc(0), P1 = gc(nb);
         const int pw0 = P0 + (int)((long long)(P1 - P0) * warp / NW);
         const int pw1 = P0 + (int)((long long)(P1 - P0) * (warp + 1) / NW);
         int cc = 0, pc = 0, pbase = pw0, cbase = pw0, pslot = 0, cslot = 0;
+        int pend = pw0, cend = pw0;  // ends (within the warp's range) of the producer's / consumer's cell
         if (pw0 < pw1) {
-            while (gcst[cc + 1] <= pw0) ++cc;
+            while (gc(cc + 1) <= pw0) ++cc;
             pc = cc;
+            pend = cend = min(gc(cc + 1), pw1);
         }
         auto issue = [&]() {
             if (pbase < pw1) {
-                const int end = min(pbase + kCcChunk, min(gcst[pc + 1], pw1));
+                const int end = min(pbase + kCcChunk, pend);
                 double2* dxy = stage_xy(pslot);
                 double* dz = stage_z(pslot);
 #pragma unroll
@@ -2137,7 +2147,14 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
                     }
                 }
                 pbase = end;
-                while (pbase < pw1 && pbase >= gcst[pc + 1]) ++pc;
+                if (pbase >= pend && pbase < pw1) {  // next non-empty cell
+                    int e;
+                    do {
+                        ++pc;
+                        e = gc(pc + 1);
+                    } while (pbase >= e);
+                    pend = min(e, pw1);
+                }
             }
             cp_async_commit();
             pslot ^= 1;
@@ -2256,7 +2273,7 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
             TRACE_DECL(tr_chunks);
             TRACE_DECL(tr_horner);
             while (cbase < pw1) {
-                const int end = min(cbase + kCcChunk, min(gcst[cc + 1], pw1));
+                const int end = min(cbase + kCcChunk, cend);
                 TRACE_CLK(tr0);
                 issue();
                 cp_async_wait<1>();
@@ -2277,7 +2294,14 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
                 TRACE_ACC(tr_chunks, 0, (end - cbase + 31) >> 5);
                 cslot ^= 1;
                 cbase = end;
-                while (cbase < pw1 && cbase >= gcst[cc + 1]) ++cc;
+                if (cbase >= cend && cbase < pw1) {
+                    int e;
+                    do {
+                        ++cc;
+                        e = gc(cc + 1);
+                    } while (cbase >= e);
+                    cend = min(e, pw1);
+                }
             }
             TRACE_PUT(1, 4, tr_wait);
             TRACE_PUT(1, 5, tr_work);

@@ -295,7 +295,7 @@ void launch_core_backward(const Geometry& g, const double* G, const double* F, d
 void launch_core_sum(const Geometry& g, int nblocks, const double* Fpart, double* F,
                      cudaStream_t s) {
     const int E = g.R * g.R * g.R + 1;
-    launch_pdl(k_core_sum, dim3((E + 7) / 8), dim3(256), 0, s, nblocks, E, Fpart, F);
+    launch_pdl_if((pdl_mask() & 4) != 0, k_core_sum, dim3((E + 7) / 8), dim3(256), 0, s, nblocks, E, Fpart, F);
     KB_CHECK_LAUNCH();
 }
 

@@ -55,7 +55,10 @@ int sm_count();
 // Programmatic dependent launch (PDL): a kernel launched with launch_pdl may
 // start while its predecessor in the stream is still running, once every CTA
 // of the predecessor has executed pdl_trigger() (or exited); it must call
-// pdl_wait() before touching anything the predecessor writes. The column
+// pdl_wait() before touching anything ANY earlier kernel of the chain writes:
+// every kernel triggers when it starts, so a kernel can be resident while a
+// kernel several links back is still running, and only plan constants (the
+// W tables, G, the cell axes) may be read before the wait. The column
 // kernels use it so that a kernel's CTAs are resident, and its table loads
 // done, when the grid-wide dependency (the summed core) arrives. Both device
 // calls are no-ops in a kernel launched the ordinary way. KPME_PDL=0 launches
@@ -69,8 +72,17 @@ inline bool pdl_enabled() {
     }();
     return on;
 }
+inline int pdl_mask() {  // debugging: KPME_PDL_MASK bit per launch site (1 z pass, 2 spread, 4 core sum, 8 gather)
+    static const int m = [] {
+        const char* e = getenv("KPME_PDL_MASK");
+        return e ? atoi(e) : 15;
+    }();
+    return m;
+}
+// `on` = false launches the ordinary way (KPME_PDL_MASK, debugging).
 template <class... KArgs, class... Args>
-void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+void launch_pdl_if(bool on, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                   Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -78,10 +90,14 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    at[0].val.programmaticStreamSerializationAllowed = on && pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     KB_CUDA(cudaLaunchKernelEx(&cfg, kern, KArgs(args)...));
+}
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    launch_pdl_if(true, kern, grid, block, smem, s, args...);
 }
 
 // Makes `device` current for one ABI call and restores the caller's current

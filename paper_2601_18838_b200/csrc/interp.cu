@@ -2048,7 +2048,10 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
                 for (int u = 0; u < WU; ++u)
                     if (u < R) wv[u] = __ldg(wsrc + (int64_t)u * g.n[2]);
             }
-            const int st0 = tid <= nb ? __ldg(a.start + cell0 + tid) : 0;
+            // The cell starts come from the sort, an earlier kernel of the launch
+            // chain: every kernel of the chain triggers its dependent when it
+            // starts, so before pdl_wait() only plan constants may be read.
+            int st0 = (!first && tid <= nb) ? __ldg(a.start + cell0 + tid) : 0;
             double4 axv = make_double4(0.0, 0.0, 0.0, 0.0);
             if (tid < nb) axv = a.cellax[2][cb0 + tid];
             if (first && fused) {
@@ -2062,7 +2065,6 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
                     wb = a.W1[(int64_t)(tid / L) * g.n[1] + cr.c1 * L + tid % L];
                 }
             }
-            if (tid <= nb) gcst[tid] = st0;
             if (tid < nb) gax[tid] = axv;
             if (w2_regs) {
                 if (tid < nz) {
@@ -2078,6 +2080,7 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
                 // Everything above is independent of the summed core: under a
                 // programmatic dependent launch it ran while the core sum did.
                 pdl_wait();
+                if (tid <= nb) st0 = __ldg(a.start + cell0 + tid);
                 double fq = 0.0;  // sum q (the last core entry), for the zero mode
                 if (tid == 0) fq = __ldcg(a.Fc + R3);
                 // zero mode, exactly: h[0] = (G[0] - c) sum q
@@ -2103,12 +2106,14 @@ __global__ void __launch_bounds__(128, MINB) k_gather_cc(ColumnArgs a, int cells
                 }
             } else if (first) {
                 pdl_wait();
+                if (tid <= nb) st0 = __ldg(a.start + cell0 + tid);
                 corr = a.corr ? *a.corr : 0.0;
                 for (int e = tid; e < L2 * R; e += NTH) {
                     const int ij = e / R, r = e % R, i = ij / L, j = ij % L;
                     b2s[e] = a.B2[((int64_t)(cr.c0 * L + i) * g.n[1] + cr.c1 * L + j) * R + r];
                 }
             }
+            if (tid <= nb) gcst[tid] = st0;
         }
         __syncthreads();
         if (first) TRACE_MARK(1, 7);
@@ -2393,15 +2398,15 @@ bool launch_spread_f8_t(const ColumnArgs& a, bool want_fwd, cudaStream_t s) {
         const bool waves = grid > 2 * 3 * sm_count() && smem * 4 <= 220 * 1024;
         // n-tiles of the W2 contraction over r = 1 .. R-1
         if (a.g.R <= 9 && waves)
-            launch_pdl(k_spread_f8<L, 1, 4>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
+            launch_pdl_if((pdl_mask() & 2) != 0, k_spread_f8<L, 1, 4>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
         else if (a.g.R <= 9)
-            launch_pdl(k_spread_f8<L, 1, 3>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
+            launch_pdl_if((pdl_mask() & 2) != 0, k_spread_f8<L, 1, 3>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
         else if (a.g.R <= 17 && waves)
-            launch_pdl(k_spread_f8<L, 2, 4>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
+            launch_pdl_if((pdl_mask() & 2) != 0, k_spread_f8<L, 2, 4>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
         else if (a.g.R <= 17)
-            launch_pdl(k_spread_f8<L, 2, 3>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
+            launch_pdl_if((pdl_mask() & 2) != 0, k_spread_f8<L, 2, 3>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
         else
-            launch_pdl(k_spread_f8<L, 4, 3>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
+            launch_pdl_if((pdl_mask() & 2) != 0, k_spread_f8<L, 4, 3>, dim3(grid), dim3(32 * F8_NW), smem, s, a, want_fwd ? 1 : 0);
         KB_CHECK_LAUNCH();
         return true;
     } else {
@@ -2500,13 +2505,13 @@ void launch_gather_t(const ColumnArgs& a0, int mode, cudaStream_t s) {
                 });
                 const bool waves = grid > 2 * 3 * sm_count() && csm * 4 <= 220 * 1024;
                 if (R == 9 && waves)
-                    launch_pdl(k_gather_cc<L, 4, 9>, dim3(grid), dim3(128), csm, s, a, ccb);
+                    launch_pdl_if((pdl_mask() & 8) != 0, k_gather_cc<L, 4, 9>, dim3(grid), dim3(128), csm, s, a, ccb);
                 else if (R == 9)
-                    launch_pdl(k_gather_cc<L, 3, 9>, dim3(grid), dim3(128), csm, s, a, ccb);
+                    launch_pdl_if((pdl_mask() & 8) != 0, k_gather_cc<L, 3, 9>, dim3(grid), dim3(128), csm, s, a, ccb);
                 else if (waves)
-                    launch_pdl(k_gather_cc<L, 4, 0>, dim3(grid), dim3(128), csm, s, a, ccb);
+                    launch_pdl_if((pdl_mask() & 8) != 0, k_gather_cc<L, 4, 0>, dim3(grid), dim3(128), csm, s, a, ccb);
                 else
-                    launch_pdl(k_gather_cc<L, 3, 0>, dim3(grid), dim3(128), csm, s, a, ccb);
+                    launch_pdl_if((pdl_mask() & 8) != 0, k_gather_cc<L, 3, 0>, dim3(grid), dim3(128), csm, s, a, ccb);
                 KB_CHECK_LAUNCH();
                 return;
             }

@@ -1461,7 +1461,7 @@ static bool launch_sort2_tiles(const Geometry& g, int64_t n, const double* xyz, 
 #ifdef ZKO_NOSP  // profiling ablation only: no record write-out (results invalid)
         sp = nullptr;
 #endif
-        launch_pdl(zk, dim3(ncol), dim3(kZThreads), kzsmem, s, g, n, ntiles, tile, pcap, b.hist, pairs, xyz, q,
+        launch_pdl_if((pdl_mask() & 1) != 0, zk, dim3(ncol), dim3(kZThreads), kzsmem, s, g, n, ntiles, tile, pcap, b.hist, pairs, xyz, q,
                    b.perm, b.start, sp);
         KB_CHECK_LAUNCH();
         if (launches) *launches += l + 1;

@@ -517,6 +517,49 @@ def test_e2e_clustered_cells(oracle, order):
     assert rel(z, oracle.kpme_apply(pb)) <= E2E_TOL
 
 
+@pytest.mark.parametrize("order,modes,counts,n", [
+    (6, 4, (2, 2, 40), 12800),   # 40 cells per column: three coefficient batches per column
+    (6, 4, (3, 3, 30), 21600),   # 30 cells: one batch at the table limit
+    (4, 3, (3, 3, 3), 2700),     # R = 7: the run-time-R expansions
+    (8, 5, (3, 2, 3), 1800),     # R = 11, L = 8
+    (6, 2, (2, 3, 4), 2400),     # R = 5
+])
+def test_gather_cell_chunk_shapes(oracle, order, modes, counts, n):
+    """The cell-chunk gather (k_gather_cc: cells of >= 64 particles on average)
+    over several batches per column, at the table limit, and for R != 9,
+    against the oracle; also with the upper half of every column empty."""
+    from oracle.binding import make_problem
+
+    pb = make_problem(oracle, n=n, counts=counts, order=order, modes=modes, eps=1e-8,
+                      seed=order + modes, charges="neutral")
+    plan = plan_for(pb)
+    z = plan.execute(dev(pb.pos), dev(pb.q)).cpu().numpy()
+    assert rel(z, oracle.kpme_apply(pb)) <= E2E_TOL
+    pos = np.array(pb.pos)
+    pos[:, 2] *= 0.5  # the cells with z >= 0.5 are empty
+    pb.pos = pos
+    z = plan.execute(dev(pb.pos), dev(pb.q)).cpu().numpy()
+    assert rel(z, oracle.kpme_apply(pb)) <= E2E_TOL
+
+
+def test_gather_cell_chunk_forced_on_sparse_cells():
+    """KPME_GATHER_CC=1 forces the cell-chunk gather where cells hold few
+    particles (one- and two-round chunks, many empty cells): every order and
+    shape of the end-to-end order tests, the water systems and the chunked host
+    path. The switch is read once per process, hence the subprocess."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KPME_GATHER_CC="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
+                        "tests/test_gpu_parity.py", "-k",
+                        "test_e2e_orders or water or chunk_edges or host_path_chunks or cfg2_vs"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
+
 @pytest.mark.parametrize("variant", ["0", "1", "1k", "1kd"])
 def test_sort_variants_forced(variant):
     """The cell-sort variants of sort2.cu -- column scatter ("0"), tile sort

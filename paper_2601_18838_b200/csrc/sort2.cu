@@ -502,10 +502,14 @@ __device__ __forceinline__ void z_whole_body(const Geometry& g, int col, int cs,
 __device__ __forceinline__ double4 gather_rec(const double* __restrict__ xyz, const double* __restrict__ q,
                                               int64_t i) {
     const double* base = xyz + 3 * i;
+#ifdef REC_LD4  // A/B: three 8-byte loads for (x, y, z)
+    return make_double4(__ldg(base), __ldg(base + 1), __ldg(base + 2), q ? __ldg(q + i) : 0.0);
+#else
     const int odd = (int)((reinterpret_cast<uintptr_t>(base) >> 3) & 1);
     const double2 v = __ldg(reinterpret_cast<const double2*>(base + odd));
     const double s = __ldg(base + (odd ? 0 : 2));
     return make_double4(odd ? s : v.x, odd ? v.x : v.y, odd ? v.y : s, q ? __ldg(q + i) : 0.0);
+#endif
 }
 // The key path (k_z_tiles_ko): staged (particle, c2) pairs; the records are
 // gathered from the input arrays (L2-resident after the tile pass) straight

@@ -420,7 +420,8 @@ def run_ours(a):
 
     clocks = Clocks(local)
     clocks.start()
-    for _ in range(max(a.warmup, 3)):
+    for _ in range(max(a.warmup, 3)):  # the warm-up steps run the timed loop's pattern: flush, then step
+        flush.zero_()
         step()
     torch.cuda.synchronize()
     if dist.is_initialized():

@@ -315,7 +315,11 @@ def ncu_traffic(kernel_key):
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get("kernels", {}).get(kernel_key, {}).get("dram_bytes")
+        k = d.get("kernels", {})
+        if kernel_key == "k_sort_stage":  # the stage's two kernels (key path)
+            parts = [k.get(n, {}).get("dram_bytes") for n in ("k_tile_keys", "k_z_tiles_ko")]
+            return sum(parts) if all(p is not None for p in parts) else None
+        return k.get(kernel_key, {}).get("dram_bytes")
     except (OSError, ValueError):
         return None
 
